@@ -1,0 +1,159 @@
+/*
+ * libccm.h -- C ABI of the B200-native all-pairs Convergent Cross Mapping hot path
+ * (mpEDM, arXiv 2011.11082; "Paper" = PAPER.md, cited as P:<line>).
+ *
+ * The calls follow the paper's problem statement: input an L x N dataset ts, the maximum
+ * embedding dimension E_max and the lag tau; output the N x N causal
+ * map rho. Phase 1 picks each series' optimal E by simplex projection
+ * (Alg. 1 lines 2-10); phase 2 builds each library series' kNN tables once and
+ * reuses them for every target (Alg. 2).
+ *
+ * Conventions (all calls):
+ *  - Every data pointer is a DEVICE pointer (cudaMalloc / PyTorch CUDA tensor) unless the
+ *    name ends in _host. Memory is caller-allocated and caller-owned: libccm never frees,
+ *    retains or aliases a pointer after the call returns.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream). Arguments are validated
+ *    synchronously; on EDM_OK all GPU work is enqueued on `stream` and the call returns
+ *    without waiting for it (device faults surface at the caller's next synchronisation).
+ *    Exception: edm_ccm_all_pairs / edm_simplex_optimal_E copy the small per-series E[]
+ *    vector to the host to validate and plan (one stream synchronisation per call).
+ *  - Indices are 0-based. Time labels: an embedded point is labelled by its
+ *    latest time t, p(t) = (x[t], x[t-tau], ..., x[t-(E-1)tau]).
+ *  - Undefined skill (a constant target) is a quiet NaN, never an error.
+ *  - No global mutable state except the thread-local last-error string; reentrant on
+ *    distinct streams and workspaces; deterministic (bit-identical reruns, and rho is
+ *    independent of how library rows are split across calls or GPUs).
+ *  - Requires an sm_100 device (B200); otherwise EDM_EUNSUPPORTED.
+ *  - Limits of this build: 1 <= E <= EDM_E_CAP (20, the paper's "<= 20 in practice",
+ *    P:377), 2 <= L, tau >= 1, Tp >= 0.
+ */
+#ifndef LIBCCM_H
+#define LIBCCM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EDM_E_CAP 20
+
+typedef enum {
+    EDM_OK = 0,
+    EDM_EINVAL = -1,      /* null pointer, bad size/range, E outside [1, EDM_E_CAP] */
+    EDM_ETOOSHORT = -2,   /* (E-1)tau+Tp >= L, or fewer than E+1 candidate points */
+    EDM_EWORKSPACE = -3,  /* ws_bytes < edm_workspace_bytes(...) */
+    EDM_ECUDA = -4,       /* a CUDA runtime/launch error (message in edm_last_error) */
+    EDM_EUNSUPPORTED = -5 /* not an sm_100 device */
+} edm_status;
+
+typedef enum {
+    EDM_E_TARGET = 0, /* paper Alg. 1/2: the table is built at optE[target] */
+    EDM_E_LIBRARY = 1 /* north_star wording: the table is built at optE[library] */
+} edm_e_mode;
+
+/* A float32 dataset in device memory, time-major: value of series j at time t is
+ * data[t * ld + j], 0 <= t < L, 0 <= j < N, ld >= N ("an L x N array ts"). */
+typedef struct {
+    const float *data;
+    int32_t N, L;
+    int64_t ld;
+} edm_dataset;
+
+/* kNN table of one series in the phase-2 form (library = target = series, Alg. 2 line 5
+ * "kNN(ts[i], ts[i], E)"; Alg. 3), at a fixed E.
+ *   series : device float[L].
+ *   rows   : n_E = L - (E-1)tau - Tp, row r <-> point t = (E-1)tau + r (points whose
+ *            future t+Tp exists).
+ *   idx    : device int32[n_E * (E+1)], row-major; the E+1 nearest candidate labels s of
+ *            row t, candidates P_E minus {t} when exclude_self, sorted by
+ *            (squared distance, s) ascending -- lowest index wins exact ties.
+ *            Bit-exact with the fp64 oracle: distances are accumulated in fp64 in the
+ *            order m = 0..E-1 with separately rounded sub/mul/add.
+ *   dist   : device float[n_E * (E+1)], Euclidean distance, fp32(sqrt(fp64 d2)).
+ *   w      : device float[n_E * (E+1)] or NULL: exponential weights u=exp(-d/d1) (d1>0)
+ *            or [d==0] (d1==0), floored at 1e-6, normalised per row.
+ * Errors: EINVAL, ETOOSHORT (n_E - exclude_self < E+1), EUNSUPPORTED, ECUDA. */
+edm_status edm_embed_knn(const float *series, int32_t L, int32_t E, int32_t tau, int32_t Tp,
+                         int32_t exclude_self, int32_t *idx, float *dist, float *w, void *stream);
+
+/* Phase 1 (Alg. 1 lines 2-10) for series [s_begin, s_end) of ds.
+ * Each series is split into library = first ceil(L/2) samples and target = the rest
+ * (P:359-360); for E = 1..E_max the target points are forecast one step
+ * ahead (Tp = 1) from their E+1 nearest library points; rho(E) = Pearson of
+ * forecast and observation; optE = argmax_E rho(E), ties -> smaller E, NaN never wins,
+ * all-NaN -> 1.
+ *   optE : device int32[s_end - s_begin]; bit-exact with the oracle (fp64 distances,
+ *          weights, forecasts and two-pass Pearson in the oracle's operation order).
+ *   rhoE : device float[(s_end - s_begin) * E_max] or NULL; row-major [series][E-1];
+ *          NaN where rho(E) is undefined (too few points, or zero variance).
+ *   workspace / ws_bytes : device scratch of at least edm_workspace_bytes(0, ...).
+ * Errors: EINVAL (E_max outside [1, EDM_E_CAP], bad range), EWORKSPACE, EUNSUPPORTED, ECUDA. */
+edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int32_t s_begin,
+                                 int32_t s_end, int32_t *optE, float *rhoE, void *workspace,
+                                 size_t ws_bytes, void *stream);
+
+/* Phase 2 (Alg. 2 lines 8-11) for library rows [lib_begin, lib_end):
+ *   rho[(i - lib_begin) * N + j] = Pearson(prediction of series j from the kNN table of
+ *   series i, observed j) = skill of cross-mapping j from i's manifold ("j CCM-causes i",
+ *   P:272-273). The diagonal i = j is computed too.
+ *   E    : device int32[N], each in [1, EDM_E_CAP] (the optE of phase 1).
+ *   mode : EDM_E_TARGET -> table at E[j] for target j; EDM_E_LIBRARY -> at E[i].
+ *   Tp   : horizon; prediction p(t) = sum_k w_k y_j[s_k + Tp], observed y_j[t + Tp],
+ *          t in P_E = [(E-1)tau, L-1-Tp].
+ *   rho  : device float[(lib_end - lib_begin) * N]; within 1e-4 of the fp64 oracle (the
+ *          kNN indices are bit-exact; the lookup and moments are fp32/fp64).
+ *   workspace / ws_bytes : device scratch of at least edm_workspace_bytes(1, ...).
+ * Errors: EINVAL, ETOOSHORT (some E[j] leaves fewer than E+1 candidates), EWORKSPACE,
+ * EUNSUPPORTED, ECUDA. */
+edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t *E, int32_t tau, int32_t Tp,
+                             edm_e_mode mode, int32_t exclude_self, int32_t lib_begin,
+                             int32_t lib_end, float *rho, void *workspace, size_t ws_bytes,
+                             void *stream);
+
+/* Scratch size in bytes for which = 0 (edm_simplex_optimal_E over N series) or
+ * which = 1 (edm_ccm_all_pairs over an N-series dataset; E_max = largest E in E[]).
+ * Returns 0 for invalid arguments. */
+size_t edm_workspace_bytes(int32_t which, int32_t N, int32_t L, int32_t E_max, int32_t tau,
+                           int32_t Tp);
+
+/* End-to-end causal map from HOST memory (the public one-call API): copies the L x N
+ * time-major float32 dataset host_data[t * N + j] to the current device, runs phase 1
+ * over all series, then phase 2 over all library rows, and copies the results back.
+ *   host_optE : int32[N] or NULL;  host_rho : float[N * N] (row = library);
+ *   host_rhoE : float[N * E_max] or NULL.
+ * Blocking; allocates and frees its own device memory. Same errors as above. */
+edm_status edm_causal_map_host(const float *host_data, int32_t N, int32_t L, int32_t E_max,
+                               int32_t tau, int32_t Tp, edm_e_mode mode, int32_t exclude_self,
+                               int32_t *host_optE, float *host_rho, float *host_rhoE);
+
+/* Thread-local message describing the last non-OK status returned on this thread. */
+const char *edm_last_error(void);
+
+/* Optional per-thread profiling of libccm's own kernel launches (used by bench.py to time
+ * the dominant kernel live with CUDA events on the launching stream). Between begin and end
+ * every launch made by libccm on this thread is bracketed by a cudaEvent pair on its stream
+ * and counted by kind. edm_profile_end waits for the recorded events and returns, per kind,
+ * the summed device milliseconds ms[k] and the launch count launches[k] (arrays of
+ * EDM_PROF_KINDS, either may be NULL). Events add ~1 us of host time per launch. */
+#define EDM_PROF_KINDS 6
+enum {
+    EDM_PROF_PREP = 0,        /* transposes, target ordering, centring, window sums */
+    EDM_PROF_SIMPLEX_KNN = 1, /* phase-1 distance + select + forecast */
+    EDM_PROF_SIMPLEX_RHO = 2, /* phase-1 Pearson + argmax */
+    EDM_PROF_CCM_KNN = 3,     /* phase-2 distance + select + weights -> tables */
+    EDM_PROF_LOOKUP = 4,      /* phase-2 lookup + fused Pearson */
+    EDM_PROF_OTHER = 5        /* edm_embed_knn */
+};
+edm_status edm_profile_begin(void);
+edm_status edm_profile_end(double *ms, int64_t *launches);
+
+/* Build identification ("libccm <version> sm_100a ..."). */
+const char *edm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LIBCCM_H */

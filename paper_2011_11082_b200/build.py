@@ -1,0 +1,52 @@
+"""Build libccm.so (the C-ABI library of include/libccm.h) in-tree with nvcc for sm_100a.
+
+No JIT cache, no torch extension: a plain `nvcc -shared` so the .so travels with the repo
+snapshot to the GPU box and is the one the tests/bench load (paper_2011_11082_b200/lib/libccm.so).
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+LIB = os.path.join(PKG, "lib", "libccm.so")
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    # no fast-math, no FMA contraction: the fp64 distance / forecast / Pearson code relies on
+    # separately rounded IEEE ops (explicit fmaf() is still used where contraction is wanted)
+    "-fmad=false",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+
+def sources():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h"))
+    return any(os.path.getmtime(p) > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if force or _stale():
+        cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", LIB + ".tmp", *sources()]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        os.makedirs(os.path.dirname(LIB), exist_ok=True)
+        subprocess.check_call(cmd)
+        os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force=True, verbose=True))

@@ -1,0 +1,458 @@
+// ccm_kernels.cuh -- sm_100a kernels of the all-pairs CCM hot path (mpEDM, arXiv 2011.11082).
+//
+// Paper = PAPER.md; P:<line>. Kernel map:
+//   transpose_kernel      time-major [L][ld] -> series-major [n][L]           (S0 ingest)
+//   colprep_kernel        per-series fp64 mean and last-change index            (S5)
+//   permute_kernel        centred, E-sorted, tile-padded time-major copy Yp     (S5)
+//   stats_kernel          per (E, column) fp64 sums of the observed window      (S5)
+//   knn_kernel<MODE>      fp64 incremental-over-E distances + warp top-(E+1)   (S1/S6/S7/S8)
+//                         MODE_CCM: weights -> table; MODE_SIMPLEX: forecast;
+//                         MODE_EMBED: idx/dist/w of edm_embed_knn
+//   simplex_rho_kernel    two-pass fp64 Pearson of the phase-1 forecasts        (S2)
+//   argmax_kernel         optE = argmax_E rho(E)                                (S3)
+//   lookup_kernel<TILE>   gather-weighted lookup + fused Pearson moments        (S9)
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace ccm {
+
+constexpr int ECAP = 20;            // largest E (k = E + 1 <= 21 <= 32 lanes)
+constexpr int TILE_J = 32;          // targets per lookup tile (one per lane)
+constexpr int KNN_WARPS = 8;        // warps per knn CTA
+constexpr int KNN_QPW = 8;          // queries per warp per CTA
+constexpr int KNN_QPB = KNN_WARPS * KNN_QPW;
+constexpr int LOOKUP_WARPS = 16;    // warps per lookup CTA (one library each)
+constexpr unsigned FULL = 0xffffffffu;
+
+enum { MODE_CCM = 0, MODE_SIMPLEX = 1, MODE_EMBED = 2 };
+
+__host__ __device__ constexpr int kpad(int k) { return (k + 1) & ~1; }
+
+// ------------------------------------------------------------------ S0 ingest
+// out[c][t] = in[t * ld + c0 + c] for c < ncols; 32x32 tiles through shared memory.
+__global__ void transpose_kernel(const float* __restrict__ in, int64_t ld, int L, int c0, int ncols,
+                                 float* __restrict__ out) {
+    __shared__ float tile[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    const int cb = blockIdx.x * 32, tb = blockIdx.y * 32;
+    for (int i = ty; i < 32; i += 8) {
+        int t = tb + i, c = cb + tx;
+        tile[i][tx] = (t < L && c < ncols) ? in[(int64_t)t * ld + c0 + c] : 0.f;
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+        int c = cb + i, t = tb + tx;
+        if (c < ncols && t < L) out[(int64_t)c * L + t] = tile[tx][i];
+    }
+}
+
+// ------------------------------------------------------------------ S5 target preparation
+// mean[j] = fp64 mean of series j; lastdiff[j] = largest t with y[t] != y[L-1] (-1 if constant).
+__global__ void colprep_kernel(const float* __restrict__ y, int64_t ld, int N, int L,
+                               double* __restrict__ mean, int* __restrict__ lastdiff) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= N) return;
+    double s = 0.0;
+    for (int t = 0; t < L; ++t) s += (double)y[(int64_t)t * ld + j];
+    mean[j] = s / L;
+    const float last = y[(int64_t)(L - 1) * ld + j];
+    int ld_ = -1;
+    for (int t = L - 2; t >= 0; --t)
+        if (y[(int64_t)t * ld + j] != last) { ld_ = t; break; }
+    lastdiff[j] = ld_;
+}
+
+// Yp[t][p] = y[t][colmap[p]] - mean[colmap[p]] (0 for padding columns colmap[p] < 0).
+// Also lastdiff_p[p] = lastdiff[colmap[p]] (-1 for padding).
+__global__ void permute_kernel(const float* __restrict__ y, int64_t ld, int L, int Np,
+                               const int* __restrict__ colmap, const double* __restrict__ mean,
+                               const int* __restrict__ lastdiff, float* __restrict__ Yp,
+                               int* __restrict__ lastdiff_p) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= Np) return;
+    const int c = colmap[p];
+    const double mu = c >= 0 ? mean[c] : 0.0;
+    if (blockIdx.y == 0) lastdiff_p[p] = c >= 0 ? lastdiff[c] : -1;
+    for (int t = blockIdx.y; t < L; t += gridDim.y)
+        Yp[(int64_t)t * Np + p] = c >= 0 ? (float)((double)y[(int64_t)t * ld + c] - mu) : 0.f;
+}
+
+// Observed-window sums for every E: the observation of row t is y[t+Tp], t in
+// P_E = [(E-1)tau, L-1-Tp], i.e. the suffix y[(E-1)tau+Tp .. L-1].
+// stats[(E-1)*Np + p] = (sum y, sum y^2) over that suffix of the centred fp32 column.
+__global__ void stats_kernel(const float* __restrict__ Yp, int L, int Np, int tau, int Tp, int Emax,
+                             double2* __restrict__ stats) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= Np) return;
+    double s1 = 0.0, s2 = 0.0;
+    int e = Emax;  // next E to record, descending: start index (e-1)tau+Tp increases with e
+    for (; e >= 1 && (e - 1) * tau + Tp > L - 1; --e)  // empty window: infeasible E
+        stats[(int64_t)(e - 1) * Np + p] = make_double2(0.0, 0.0);
+    for (int t = L - 1; t >= 0 && e >= 1; --t) {
+        const double v = (double)Yp[(int64_t)t * Np + p];
+        s1 += v;
+        s2 += v * v;
+        while (e >= 1 && t == (e - 1) * tau + Tp) {
+            stats[(int64_t)(e - 1) * Np + p] = make_double2(s1, s2);
+            --e;
+        }
+    }
+    for (; e >= 1; --e) stats[(int64_t)(e - 1) * Np + p] = make_double2(0.0, 0.0);  // infeasible E
+}
+
+// ------------------------------------------------------------------ kNN (S1/S6, S7, S8)
+struct KnnParams {
+    const float* X;         // series-major rows (MODE_CCM/SIMPLEX) or the single series (EMBED)
+    int64_t ldx;            // row stride of X
+    const int* slot_series; // X row of block slot b (NULL: b)
+    int L, tau, Tp, excl;
+    unsigned maskS;         // bit E set <=> a list is kept at E (target mode / simplex / embed)
+    int Etop;               // largest E needed
+    const int* slotE;       // library mode: E of slot b (overrides maskS/Etop); NULL otherwise
+    // MODE_CCM output: tables[b * T_lib + offE[E] + row * kpad(E+1) + j] = {s + Tp, w bits}
+    uint2* tables;
+    int64_t T_lib;
+    int64_t offE[ECAP + 2];
+    // MODE_SIMPLEX output: pred[(b * ECAP + E-1) * LQ + t] (fp64 forecast of target point t)
+    double* pred;
+    int LQ;
+    // MODE_EMBED output (rows t - (E-1)tau, k columns)
+    int* out_idx;
+    float* out_dist;
+    float* out_w;
+};
+
+__device__ __forceinline__ int hi_word(double d) { return __double2hiint(d); }
+
+// Insert every lane flagged in `bal` into the warp-distributed sorted list (lane j holds
+// entry j, lanes >= k hold +inf). Candidates arrive in increasing s (lanes low -> high,
+// chunks in order), so an entry already in the list with an equal distance has a smaller
+// index and stays in front: the (d2, s) lexicographic order of C4 / S:137.
+__device__ __forceinline__ void list_insert(unsigned bal, double D, int s, int k, int lane,
+                                            double& Ld, int& Ls, int& thr) {
+    while (bal) {
+        const int src = __ffs(bal) - 1;
+        bal &= bal - 1;
+        const double Dn = __shfl_sync(FULL, D, src);
+        const int sn = __shfl_sync(FULL, s, src);
+        const double th = __shfl_sync(FULL, Ld, k - 1);
+        if (Dn < th) {
+            const int pos = __popc(__ballot_sync(FULL, Ld <= Dn));
+            const double ud = __shfl_up_sync(FULL, Ld, 1);
+            const int us = __shfl_up_sync(FULL, Ls, 1);
+            if (lane > pos) { Ld = ud; Ls = us; }
+            if (lane == pos) { Ld = Dn; Ls = sn; }
+            if (lane >= k) { Ld = CUDART_INF; Ls = 0x7fffffff; }
+            thr = hi_word(__shfl_sync(FULL, Ld, k - 1));
+        }
+    }
+}
+
+// Weights of C5: lane j < k holds d2_j. Returns w_j (0 for lanes >= k).
+// exact == true: fp64 exp and the oracle's sequential normalisation order;
+// exact == false (phase-2 tables, stored as fp32): fp32 exp and a tree sum.
+template <bool EXACT>
+__device__ __forceinline__ double simplex_weight(double d2, int k, int lane) {
+    const double d = lane < k ? sqrt(d2) : 0.0;
+    const double d1 = __shfl_sync(FULL, d, 0);
+    double u;
+    if (d1 > 0.0) u = EXACT ? exp(__ddiv_rn(-d, d1)) : (double)__expf(-(float)__ddiv_rn(d, d1));
+    else u = (d == 0.0) ? 1.0 : 0.0;
+    if (u < 1e-6) u = 1e-6;
+    if (lane >= k) u = 0.0;
+    double sum = 0.0;
+    if (EXACT) {
+        for (int j = 0; j < k; ++j) sum = __dadd_rn(sum, __shfl_sync(FULL, u, j));
+    } else {
+        sum = u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+    }
+    return __ddiv_rn(u, sum);
+}
+
+// One query point t (one warp): D_E(t, s) for E = 1..Eq accumulated incrementally over E
+// (D_E = D_{E-1} + (a[t-(E-1)tau] - b[s-(E-1)tau])^2, the same fp64 operation sequence as
+// the oracle's C3 loop, so every D_E is bit-identical to the oracle's), and at every E in the
+// selected set a top-(E+1) list by (D_E, s).
+template <int MODE>
+__device__ __forceinline__ void knn_query(const KnnParams& P, const double* __restrict__ qa,
+                                          const double* __restrict__ cb, int t, int ncand,
+                                          unsigned mask, int Etop, int b, int lane) {
+    const int tau = P.tau;
+    const int Eq = min(Etop, t / tau + 1);  // E with (E-1) tau <= t
+    const bool excl = (MODE != MODE_SIMPLEX) && P.excl;
+    double q[ECAP];
+    double Ld[ECAP];
+    int Ls[ECAP], thr[ECAP];
+#pragma unroll
+    for (int e = 0; e < ECAP; ++e) {
+        q[e] = (e < Eq) ? qa[t - e * tau] : 0.0;
+        Ld[e] = CUDART_INF;
+        Ls[e] = 0x7fffffff;
+        thr[e] = 0x7ff00000;  // hi word of +inf
+    }
+    for (int c0 = 0; c0 < ncand; c0 += 32) {
+        const int s = c0 + lane;
+        const bool valid = (s < ncand) && !(excl && s == t);
+        double D = 0.0;
+#pragma unroll
+        for (int e = 0; e < ECAP; ++e) {
+            if (e < Eq) {
+                const int sm = s - e * tau;
+                const bool ve = valid && sm >= 0;
+                const double xv = cb[max(min(sm, ncand - 1), 0)];
+                const double diff = __dsub_rn(q[e], xv);
+                D = __dadd_rn(D, __dmul_rn(diff, diff));
+                if ((mask >> (e + 1)) & 1u) {
+                    // prefilter on the high word: D < theta implies hi(D) <= hi(theta) (D >= 0)
+                    const unsigned bal = __ballot_sync(FULL, ve && hi_word(D) <= thr[e]);
+                    if (bal) list_insert(bal, D, s, e + 2, lane, Ld[e], Ls[e], thr[e]);
+                }
+            }
+        }
+    }
+    // finalise every selected E of this query
+#pragma unroll
+    for (int e = 0; e < ECAP; ++e) {
+        if (e < Eq && ((mask >> (e + 1)) & 1u)) {
+            const int k = e + 2;
+            const int row = t - e * tau;
+            if (MODE == MODE_CCM) {
+                const double w = simplex_weight<false>(Ld[e], k, lane);
+                const int kp = kpad(k);
+                if (lane < kp) {
+                    uint2 ent = lane < k ? make_uint2((unsigned)(Ls[e] + P.Tp), __float_as_uint((float)w))
+                                         : make_uint2(0u, 0u);
+                    P.tables[(int64_t)b * P.T_lib + P.offE[e + 1] + (int64_t)row * kp + lane] = ent;
+                }
+            } else if (MODE == MODE_EMBED) {
+                const double w = simplex_weight<true>(Ld[e], k, lane);
+                if (lane < k) {
+                    P.out_idx[(int64_t)row * k + lane] = Ls[e];
+                    P.out_dist[(int64_t)row * k + lane] = (float)sqrt(Ld[e]);
+                    if (P.out_w) P.out_w[(int64_t)row * k + lane] = (float)w;
+                }
+            } else {  // MODE_SIMPLEX: forecast one step ahead, yhat = sum_k w_k lib[s_k + 1]
+                const double w = simplex_weight<true>(Ld[e], k, lane);
+                const double prod = lane < k ? __dmul_rn(w, cb[Ls[e] + 1]) : 0.0;
+                double acc = 0.0;
+                for (int j = 0; j < k; ++j) acc = __dadd_rn(acc, __shfl_sync(FULL, prod, j));
+                if (lane == 0) P.pred[((int64_t)b * ECAP + e) * P.LQ + t] = acc;
+            }
+        }
+    }
+}
+
+// grid = (ceil(nq / KNN_QPB), slots); block = KNN_WARPS * 32; dynamic smem = L doubles.
+template <int MODE>
+__global__ void __launch_bounds__(KNN_WARPS * 32) knn_kernel(KnnParams P) {
+    extern __shared__ double xs[];
+    const int b = blockIdx.y;
+    const int row = P.slot_series ? P.slot_series[b] : b;
+    const float* xg = P.X + (int64_t)row * P.ldx;
+    for (int i = threadIdx.x; i < P.L; i += blockDim.x) xs[i] = (double)xg[i];
+    __syncthreads();
+    unsigned mask = P.maskS;
+    int Etop = P.Etop;
+    if (P.slotE) {
+        const int e = P.slotE[b];
+        mask = 1u << e;
+        Etop = e;
+    }
+    const double* qa;
+    const double* cb;
+    int nq, ncand;
+    if (MODE == MODE_SIMPLEX) {
+        const int Llib = (P.L + 1) / 2;   // library = first ceil(L/2) samples
+        cb = xs;
+        qa = xs + Llib;
+        nq = (P.L - Llib) - 1;            // target points t with t+1 inside the target half
+        ncand = Llib - 1;                 // library points s with s+1 inside the library half
+    } else {
+        qa = cb = xs;
+        nq = ncand = P.L - P.Tp;          // P_1 = [0, L-1-Tp]; per-E lower bound (E-1)tau
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t_end = min(nq, (int)(blockIdx.x + 1) * KNN_QPB);
+    for (int t = blockIdx.x * KNN_QPB + warp; t < t_end; t += KNN_WARPS)
+        knn_query<MODE>(P, qa, cb, t, ncand, mask, Etop, b, lane);
+}
+
+// ------------------------------------------------------------------ S2 / S3 phase-1 skill
+// rho(E) of series slot b: two-pass fp64 Pearson of (pred[t], tgt[t+1]) over the query rows
+// t in [(E-1)tau, Ltgt-2], in the oracle's order (C7); NaN if infeasible or constant.
+__global__ void simplex_rho_kernel(const float* __restrict__ X, int64_t ldx, const double* __restrict__ pred,
+                                   int LQ, int L, int tau, int Emax, int nslots, double* __restrict__ rhoE) {
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= nslots * Emax) return;
+    const int b = gid / Emax, e = gid % Emax;
+    const int Llib = (L + 1) / 2, Ltgt = L - Llib;
+    const int lo = e * tau;
+    const int nq = Ltgt - 1 - lo, nc = Llib - 1 - lo;
+    double r = CUDART_NAN;
+    if (nc >= e + 2 && nq >= 2) {
+        const double* p = pred + ((int64_t)b * ECAP + e) * LQ + lo;
+        const float* o = X + (int64_t)b * ldx + Llib + lo + 1;
+        bool pc = true, oc = true;
+        const double p0 = p[0], o0 = (double)o[0];
+        for (int i = 1; i < nq; ++i) {
+            if (p[i] != p0) pc = false;
+            if ((double)o[i] != o0) oc = false;
+        }
+        if (!pc && !oc) {
+            double sa = 0.0, sb = 0.0;
+            for (int i = 0; i < nq; ++i) { sa = __dadd_rn(sa, p[i]); sb = __dadd_rn(sb, (double)o[i]); }
+            const double ma = __ddiv_rn(sa, (double)nq), mb = __ddiv_rn(sb, (double)nq);
+            double sab = 0.0, saa = 0.0, sbb = 0.0;
+            for (int i = 0; i < nq; ++i) {
+                const double da = __dsub_rn(p[i], ma), db = __dsub_rn((double)o[i], mb);
+                sab = __dadd_rn(sab, __dmul_rn(da, db));
+                saa = __dadd_rn(saa, __dmul_rn(da, da));
+                sbb = __dadd_rn(sbb, __dmul_rn(db, db));
+            }
+            if (saa != 0.0 && sbb != 0.0) r = __ddiv_rn(sab, sqrt(__dmul_rn(saa, sbb)));
+        }
+    }
+    rhoE[gid] = r;
+}
+
+// optE = argmax_E rho(E): NaN never wins, ties -> smaller E, all NaN -> 1 (C8).
+__global__ void argmax_kernel(const double* __restrict__ rhoE, int Emax, int nslots, int* __restrict__ optE,
+                              float* __restrict__ rhoE_out) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nslots) return;
+    int best = 0;
+    double br = 0.0;
+    for (int e = 0; e < Emax; ++e) {
+        const double r = rhoE[(int64_t)b * Emax + e];
+        if (rhoE_out) rhoE_out[(int64_t)b * Emax + e] = (float)r;
+        if (!isnan(r) && (best == 0 || r > br)) { best = e + 1; br = r; }
+    }
+    optE[b] = best == 0 ? 1 : best;
+}
+
+// ------------------------------------------------------------------ S9 lookup + fused rho
+struct LookupParams {
+    const float* Yp;        // [L][Np] centred, permuted, tile-padded targets
+    int64_t Np;
+    const int* colmap;      // [Np] original column (or -1)
+    const int* tileE;       // [ntiles] E of tile (target mode) or NULL (library mode)
+    const int* slotE;       // [B] E of library slot (library mode)
+    const int* slotRow;     // [B] output row of slot (i - lib_begin)
+    const uint2* tables;
+    int64_t T_lib;
+    int64_t offE[ECAP + 2];
+    const double2* stats;   // [ECAP][Np]
+    const int* lastdiff;    // [Np] (per permuted column)
+    int L, tau, Tp, B, N;
+    float* rho;
+};
+
+// p(t) = sum_j w_j y[s_j + Tp] (Alg. 5) for the lane's target over the rows of
+// one table, with the Pearson moments sum p, sum p^2, sum p*o accumulated on the fly (fp32
+// within 32-row blocks, fp64 across blocks); o = y[t + Tp]. Then rho from the moments and the
+// precomputed fp64 sums of o (C10).
+template <int E, bool SMEM>
+__device__ __forceinline__ void lookup_one(const LookupParams& P, const float* __restrict__ Y, int64_t ys,
+                                           int tile, int b, int lane, int col) {
+    constexpr int k = E + 1, kp = kpad(k);
+    const uint4* tab = reinterpret_cast<const uint4*>(P.tables + (int64_t)b * P.T_lib + P.offE[E]);
+    const int t0 = (E - 1) * P.tau;
+    const int n = P.L - t0 - P.Tp;
+    double Sp = 0.0, Spp = 0.0, Spo = 0.0;
+    const float* Yo = Y + (int64_t)(t0 + P.Tp) * ys + lane;
+    const float* Yl = Y + lane;
+    auto predict = [&](int r) {
+        const uint4* row = tab + (int64_t)r * (kp / 2);
+        float p = 0.f;
+#pragma unroll
+        for (int j2 = 0; j2 < kp / 2; ++j2) {
+            const uint4 e2 = __ldg(row + j2);
+            p = fmaf(__uint_as_float(e2.y), Yl[(int64_t)e2.x * ys], p);
+            if (2 * j2 + 1 < k) p = fmaf(__uint_as_float(e2.w), Yl[(int64_t)e2.z * ys], p);
+        }
+        return p;
+    };
+    // moments of the prediction shifted by its first value: no cancellation when the
+    // prediction is (nearly) constant, e.g. a constant library series (all neighbours tie)
+    const float c = predict(0);
+    for (int r0 = 0; r0 < n; r0 += 32) {
+        const int r1 = min(n, r0 + 32);
+        float sp = 0.f, spp = 0.f, spo = 0.f;
+#pragma unroll 2
+        for (int r = r0; r < r1; ++r) {
+            const float p = predict(r) - c;
+            const float o = Yo[(int64_t)r * ys];
+            sp += p;
+            spp = fmaf(p, p, spp);
+            spo = fmaf(p, o, spo);
+        }
+        Sp += (double)sp;
+        Spp += (double)spp;
+        Spo += (double)spo;
+    }
+    if (col >= 0) {
+        const int pcol = tile * TILE_J + lane;
+        const double2 st = P.stats[(int64_t)(E - 1) * P.Np + pcol];
+        const bool o_const = P.lastdiff[pcol] < t0 + P.Tp;  // every observed value equal
+        const double nn = (double)n;
+        const double cov = Spo - Sp * st.x / nn;
+        const double vp = Spp - Sp * Sp / nn;
+        const double vo = st.y - st.x * st.x / nn;
+        float r = CUDART_NAN_F;
+        if (!o_const && vp > 0.0 && vo > 0.0) r = (float)(cov / sqrt(vp * vo));
+        P.rho[(int64_t)P.slotRow[b] * P.N + col] = r;
+    }
+}
+
+template <bool SMEM>
+__device__ __forceinline__ void lookup_dispatch(int E, const LookupParams& P, const float* Y, int64_t ys, int tile,
+                                                int b, int lane, int col) {
+    switch (E) {
+#define CCM_CASE(e) case e: lookup_one<e, SMEM>(P, Y, ys, tile, b, lane, col); break;
+        CCM_CASE(1) CCM_CASE(2) CCM_CASE(3) CCM_CASE(4) CCM_CASE(5) CCM_CASE(6) CCM_CASE(7)
+        CCM_CASE(8) CCM_CASE(9) CCM_CASE(10) CCM_CASE(11) CCM_CASE(12) CCM_CASE(13) CCM_CASE(14)
+        CCM_CASE(15) CCM_CASE(16) CCM_CASE(17) CCM_CASE(18) CCM_CASE(19) CCM_CASE(20)
+#undef CCM_CASE
+        default: break;
+    }
+}
+
+// grid = ntiles; block = LOOKUP_WARPS * 32. SMEM = true: the 32-column target tile
+// Yp[0..L)[tile*32 .. +32) is staged in shared memory ([L][32] fp32) once and reused by
+// every library of the block (the table reuse of Alg. 2, turned into target-tile
+// reuse); SMEM = false (long series): gathers straight from L2/HBM.
+template <bool SMEM>
+__global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupParams P) {
+    extern __shared__ float ytile[];
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int Et = P.tileE ? P.tileE[tile] : 0;
+    if (P.tileE && Et <= 0) return;
+    const float* Y;
+    int64_t ys;
+    if (SMEM) {
+        const float* src = P.Yp + (int64_t)tile * TILE_J;
+        for (int i = threadIdx.x; i < P.L * (TILE_J / 4); i += blockDim.x) {
+            const int t = i / (TILE_J / 4), c = (i % (TILE_J / 4)) * 4;
+            *reinterpret_cast<float4*>(ytile + t * TILE_J + c) =
+                __ldg(reinterpret_cast<const float4*>(src + (int64_t)t * P.Np + c));
+        }
+        __syncthreads();
+        Y = ytile;
+        ys = TILE_J;
+    } else {
+        Y = P.Yp + (int64_t)tile * TILE_J;
+        ys = P.Np;
+    }
+    const int col = P.colmap[tile * TILE_J + lane];
+    for (int b = warp; b < P.B; b += LOOKUP_WARPS) {
+        const int E = P.tileE ? Et : P.slotE[b];
+        lookup_dispatch<SMEM>(E, P, Y, ys, tile, b, lane, col);
+    }
+}
+
+}  // namespace ccm

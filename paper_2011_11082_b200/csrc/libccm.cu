@@ -1,0 +1,441 @@
+// libccm.cu -- host side of the C ABI declared in include/libccm.h: argument validation,
+// planning (target ordering, library blocks, workspace carving) and kernel launches.
+// Kernels: ccm_kernels.cuh. Paper = PAPER.md (arXiv 2011.11082), P:<line>.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ccm_kernels.cuh"
+#include "libccm.h"
+
+using namespace ccm;
+
+namespace {
+
+thread_local std::string g_err;
+
+edm_status fail(edm_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+edm_status fail(edm_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                           \
+    do {                                                                                         \
+        cudaError_t e_ = (expr);                                                                 \
+        if (e_ != cudaSuccess) return fail(EDM_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_));  \
+    } while (0)
+
+#define LAUNCH_CHECK(what)                                                                       \
+    do {                                                                                         \
+        cudaError_t e_ = cudaGetLastError();                                                     \
+        if (e_ != cudaSuccess) return fail(EDM_ECUDA, "launch %s: %s", what, cudaGetErrorString(e_)); \
+    } while (0)
+
+edm_status check_device() {
+    int dev = 0, major = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    if (major != 10) return fail(EDM_EUNSUPPORTED, "libccm is built for sm_100a; device has compute capability %d.x", major);
+    return EDM_OK;
+}
+
+
+// ---- optional per-thread profiling of libccm's own launches (edm_profile_begin/end)
+struct Prof {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<int> kind;     // per recorded launch
+    int64_t launches[EDM_PROF_KINDS] = {};
+};
+thread_local Prof g_prof;
+
+cudaEvent_t prof_event() {
+    if (g_prof.used == g_prof.pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        g_prof.pool.push_back(e);
+    }
+    return g_prof.pool[g_prof.used++];
+}
+
+// Brackets one launch with events on its stream when profiling is on; always counts it.
+#define PROF_LAUNCH(KIND, STREAM, ...)                                                          \
+    do {                                                                                         \
+        cudaEvent_t e0_ = nullptr, e1_ = nullptr;                                                \
+        if (g_prof.on) { e0_ = prof_event(); e1_ = prof_event(); }                               \
+        if (e0_) cudaEventRecord(e0_, STREAM);                                                   \
+        __VA_ARGS__;                                                                             \
+        if (e1_) { cudaEventRecord(e1_, STREAM); g_prof.kind.push_back(KIND); }                  \
+        if (g_prof.on) g_prof.launches[KIND]++;                                                  \
+    } while (0)
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// Rows of the phase-2 table at E: n_E = L - (E-1) tau - Tp.
+inline int64_t n_rows(int L, int E, int tau, int Tp) { return (int64_t)L - (int64_t)(E - 1) * tau - Tp; }
+
+// Per-library table layout: blocks for E = 1..ECAP (rows n_E, row stride kpad(E+1) entries).
+void table_layout(int L, int tau, int Tp, int64_t offE[ECAP + 2], int64_t* T_lib) {
+    int64_t off = 0;
+    offE[0] = 0;
+    for (int E = 1; E <= ECAP; ++E) {
+        offE[E] = off;
+        const int64_t n = std::max<int64_t>(n_rows(L, E, tau, Tp), 0);
+        off += n * kpad(E + 1);
+    }
+    offE[ECAP + 1] = off;
+    *T_lib = off;
+}
+
+constexpr int SIMPLEX_SLOTS = 2048;   // series per phase-1 block
+constexpr int CCM_B = LOOKUP_WARPS;   // libraries per phase-2 block (one lookup warp each)
+constexpr int LOOKUP_SMEM_MAX = 227 * 1024;
+
+inline int64_t np_max(int N) { return (int64_t)(N + TILE_J - 1) / TILE_J * TILE_J + (int64_t)TILE_J * ECAP; }
+
+struct SimplexWs {
+    float* Xs;      // [SB][L]
+    double* pred;   // [SB][ECAP][LQ]
+    double* rho;    // [SB][E_max]
+    size_t bytes;
+};
+
+SimplexWs simplex_ws(void* base, int N, int L, int E_max) {
+    SimplexWs w{};
+    const int SB = std::min(N, SIMPLEX_SLOTS);
+    const int LQ = std::max(L / 2, 1);
+    size_t off = 0;
+    char* b = (char*)base;
+    w.Xs = (float*)(b + off);   off += align_up((size_t)SB * L * sizeof(float));
+    w.pred = (double*)(b + off); off += align_up((size_t)SB * ECAP * LQ * sizeof(double));
+    w.rho = (double*)(b + off);  off += align_up((size_t)SB * std::max(E_max, 1) * sizeof(double));
+    w.bytes = off;
+    return w;
+}
+
+struct CcmWs {
+    float* Xs;          // [N][L] library series, series-major
+    float* Yp;          // [L][Npm] centred permuted targets
+    int* colmap;        // [Npm]
+    int* lastdiff_p;    // [Npm]
+    int* tileE;         // [Npm / 32]
+    double* mean;       // [N]
+    int* lastdiff;      // [N]
+    double2* stats;     // [ECAP][Npm]
+    int* slot_series;   // [N]
+    int* slot_row;      // [N]
+    int* slotE;         // [N]
+    uint2* tables;      // [CCM_B][T_lib]
+    int64_t Npm, T_lib;
+    size_t bytes;
+};
+
+CcmWs ccm_ws(void* base, int N, int L, int tau, int Tp) {
+    CcmWs w{};
+    int64_t offE[ECAP + 2];
+    table_layout(L, tau, Tp, offE, &w.T_lib);
+    w.Npm = np_max(N);
+    size_t off = 0;
+    char* b = (char*)base;
+    auto take = [&](size_t bytes) { char* p = b + off; off += align_up(bytes); return p; };
+    w.Xs = (float*)take((size_t)N * L * sizeof(float));
+    w.Yp = (float*)take((size_t)L * w.Npm * sizeof(float));
+    w.colmap = (int*)take((size_t)w.Npm * sizeof(int));
+    w.lastdiff_p = (int*)take((size_t)w.Npm * sizeof(int));
+    w.tileE = (int*)take((size_t)(w.Npm / TILE_J) * sizeof(int));
+    w.mean = (double*)take((size_t)N * sizeof(double));
+    w.lastdiff = (int*)take((size_t)N * sizeof(int));
+    w.stats = (double2*)take((size_t)ECAP * w.Npm * sizeof(double2));
+    w.slot_series = (int*)take((size_t)N * sizeof(int));
+    w.slot_row = (int*)take((size_t)N * sizeof(int));
+    w.slotE = (int*)take((size_t)N * sizeof(int));
+    w.tables = (uint2*)take((size_t)CCM_B * w.T_lib * sizeof(uint2));
+    w.bytes = off;
+    return w;
+}
+
+template <int MODE>
+edm_status launch_knn(const KnnParams& P, int nq, int slots, size_t smem, cudaStream_t st) {
+    static_assert(MODE >= 0, "");
+    if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(knn_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 grid((nq + KNN_QPB - 1) / KNN_QPB, slots);
+    PROF_LAUNCH(MODE == MODE_CCM ? EDM_PROF_CCM_KNN : MODE == MODE_SIMPLEX ? EDM_PROF_SIMPLEX_KNN : EDM_PROF_OTHER, st,
+                knn_kernel<MODE><<<grid, KNN_WARPS * 32, smem, st>>>(P));
+    LAUNCH_CHECK("knn_kernel");
+    return EDM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* edm_last_error(void) { return g_err.c_str(); }
+
+edm_status edm_profile_begin(void) {
+    g_prof.on = true;
+    g_prof.used = 0;
+    g_prof.kind.clear();
+    for (int k = 0; k < EDM_PROF_KINDS; ++k) g_prof.launches[k] = 0;
+    return EDM_OK;
+}
+
+edm_status edm_profile_end(double* ms, int64_t* launches) {
+    g_prof.on = false;
+    double acc[EDM_PROF_KINDS] = {};
+    for (size_t i = 0; i < g_prof.kind.size(); ++i) {
+        cudaEvent_t a = g_prof.pool[2 * i], b = g_prof.pool[2 * i + 1];
+        CUDA_TRY(cudaEventSynchronize(b));
+        float t = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&t, a, b));
+        acc[g_prof.kind[i]] += t;
+    }
+    for (int k = 0; k < EDM_PROF_KINDS; ++k) {
+        if (ms) ms[k] = acc[k];
+        if (launches) launches[k] = g_prof.launches[k];
+    }
+    g_prof.kind.clear();
+    g_prof.used = 0;
+    return EDM_OK;
+}
+
+const char* edm_version(void) { return "libccm 0.1 sm_100a (fp64 exact kNN, fp32 lookup)"; }
+
+size_t edm_workspace_bytes(int32_t which, int32_t N, int32_t L, int32_t E_max, int32_t tau, int32_t Tp) {
+    if (N < 1 || L < 2 || E_max < 1 || E_max > ECAP || tau < 1 || Tp < 0) return 0;
+    if (which == 0) return simplex_ws(nullptr, N, L, E_max).bytes;
+    if (which == 1) return ccm_ws(nullptr, N, L, tau, Tp).bytes;
+    return 0;
+}
+
+edm_status edm_embed_knn(const float* series, int32_t L, int32_t E, int32_t tau, int32_t Tp, int32_t exclude_self,
+                         int32_t* idx, float* dist, float* w, void* stream) {
+    if (!series || !idx || !dist) return fail(EDM_EINVAL, "null pointer");
+    if (L < 2 || E < 1 || E > ECAP || tau < 1 || Tp < 0)
+        return fail(EDM_EINVAL, "bad arguments L=%d E=%d tau=%d Tp=%d (1 <= E <= %d)", L, E, tau, Tp, ECAP);
+    const int64_t n = n_rows(L, E, tau, Tp);
+    if (n - (exclude_self ? 1 : 0) < E + 1)
+        return fail(EDM_ETOOSHORT, "n_E=%lld points leave fewer than E+1=%d candidates", (long long)n, E + 1);
+    edm_status st = check_device();
+    if (st != EDM_OK) return st;
+    KnnParams P{};
+    P.X = series;
+    P.ldx = L;
+    P.L = L; P.tau = tau; P.Tp = Tp; P.excl = exclude_self ? 1 : 0;
+    P.maskS = 1u << E;
+    P.Etop = E;
+    P.out_idx = idx; P.out_dist = dist; P.out_w = w;
+    return launch_knn<MODE_EMBED>(P, L - Tp, 1, (size_t)L * sizeof(double), (cudaStream_t)stream);
+}
+
+edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int32_t s_begin, int32_t s_end,
+                                 int32_t* optE, float* rhoE, void* workspace, size_t ws_bytes, void* stream) {
+    if (!ds.data || !optE || !workspace) return fail(EDM_EINVAL, "null pointer");
+    if (ds.N < 1 || ds.L < 2 || ds.ld < ds.N || E_max < 1 || E_max > ECAP || tau < 1)
+        return fail(EDM_EINVAL, "bad arguments N=%d L=%d ld=%lld E_max=%d tau=%d", ds.N, ds.L, (long long)ds.ld, E_max, tau);
+    if (s_begin < 0 || s_end > ds.N || s_begin > s_end) return fail(EDM_EINVAL, "bad series range [%d,%d)", s_begin, s_end);
+    const size_t need = edm_workspace_bytes(0, ds.N, ds.L, E_max, tau, 1);
+    if (ws_bytes < need) return fail(EDM_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+    edm_status st = check_device();
+    if (st != EDM_OK) return st;
+    if (s_begin == s_end) return EDM_OK;
+    cudaStream_t cs = (cudaStream_t)stream;
+    SimplexWs W = simplex_ws(workspace, ds.N, ds.L, E_max);
+    const int L = ds.L, Llib = (L + 1) / 2, Ltgt = L - Llib;
+    const int LQ = std::max(L / 2, 1);
+    // feasible E (C2): at least E+1 library candidates and 2 target queries
+    unsigned mask = 0;
+    int Etop = 0;
+    for (int E = 1; E <= E_max; ++E) {
+        const int lo = (E - 1) * tau;
+        if (Llib - 1 - lo >= E + 1 && Ltgt - 1 - lo >= 2) { mask |= 1u << E; Etop = E; }
+    }
+    const int SB = std::min(ds.N, SIMPLEX_SLOTS);
+    for (int c0 = s_begin; c0 < s_end; c0 += SB) {
+        const int nb = std::min(SB, s_end - c0);
+        dim3 tb(32, 8), tg((nb + 31) / 32, (L + 31) / 32);
+        PROF_LAUNCH(EDM_PROF_PREP, cs, transpose_kernel<<<tg, tb, 0, cs>>>(ds.data, ds.ld, L, c0, nb, W.Xs));
+        LAUNCH_CHECK("transpose_kernel");
+        if (Etop > 0) {
+            KnnParams P{};
+            P.X = W.Xs; P.ldx = L; P.L = L; P.tau = tau; P.Tp = 1; P.excl = 0;
+            P.maskS = mask; P.Etop = Etop; P.pred = W.pred; P.LQ = LQ;
+            st = launch_knn<MODE_SIMPLEX>(P, std::max(Ltgt - 1, 1), nb, (size_t)L * sizeof(double), cs);
+            if (st != EDM_OK) return st;
+        }
+        const int nthr = nb * E_max;
+        PROF_LAUNCH(EDM_PROF_SIMPLEX_RHO, cs, simplex_rho_kernel<<<(nthr + 127) / 128, 128, 0, cs>>>(W.Xs, L, W.pred, LQ, L, tau, E_max, nb, W.rho));
+        LAUNCH_CHECK("simplex_rho_kernel");
+        PROF_LAUNCH(EDM_PROF_SIMPLEX_RHO, cs,
+                    argmax_kernel<<<(nb + 127) / 128, 128, 0, cs>>>(W.rho, E_max, nb, optE + (c0 - s_begin),
+                                                                    rhoE ? rhoE + (size_t)(c0 - s_begin) * E_max : nullptr));
+        LAUNCH_CHECK("argmax_kernel");
+    }
+    return EDM_OK;
+}
+
+edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int32_t Tp, edm_e_mode mode,
+                             int32_t exclude_self, int32_t lib_begin, int32_t lib_end, float* rho, void* workspace,
+                             size_t ws_bytes, void* stream) {
+    if (!ds.data || !E || !rho || !workspace) return fail(EDM_EINVAL, "null pointer");
+    if (ds.N < 1 || ds.L < 2 || ds.ld < ds.N || tau < 1 || Tp < 0 || (mode != EDM_E_TARGET && mode != EDM_E_LIBRARY))
+        return fail(EDM_EINVAL, "bad arguments N=%d L=%d ld=%lld tau=%d Tp=%d mode=%d", ds.N, ds.L, (long long)ds.ld, tau, Tp, (int)mode);
+    if (lib_begin < 0 || lib_end > ds.N || lib_begin > lib_end) return fail(EDM_EINVAL, "bad library range [%d,%d)", lib_begin, lib_end);
+    const size_t need = edm_workspace_bytes(1, ds.N, ds.L, ECAP, tau, Tp);
+    if (need == 0 || ws_bytes < need) return fail(EDM_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+    edm_status st = check_device();
+    if (st != EDM_OK) return st;
+    cudaStream_t cs = (cudaStream_t)stream;
+    const int N = ds.N, L = ds.L;
+
+    // ---- validate E[] and plan on the host (one small D2H copy)
+    std::vector<int32_t> hE(N);
+    CUDA_TRY(cudaMemcpyAsync(hE.data(), E, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, cs));
+    CUDA_TRY(cudaStreamSynchronize(cs));
+    unsigned maskS = 0;
+    int Etop = 0;
+    for (int j = 0; j < N; ++j) {
+        const int e = hE[j];
+        if (e < 1 || e > ECAP) return fail(EDM_EINVAL, "E[%d]=%d outside [1,%d]", j, e, ECAP);
+        if (n_rows(L, e, tau, Tp) - (exclude_self ? 1 : 0) < e + 1)
+            return fail(EDM_ETOOSHORT, "E[%d]=%d leaves fewer than E+1 candidates at L=%d tau=%d Tp=%d", j, e, L, tau, Tp);
+        maskS |= 1u << e;
+        Etop = std::max(Etop, e);
+    }
+    if (lib_begin == lib_end) return EDM_OK;
+    CcmWs W = ccm_ws(workspace, N, L, tau, Tp);
+    int64_t offE[ECAP + 2], T_lib;
+    table_layout(L, tau, Tp, offE, &T_lib);
+
+    // target ordering (S5): target mode -> stable counting sort by (E_j, j), every E segment
+    // padded to a multiple of 32 so that a 32-target tile has one E; library mode -> identity.
+    std::vector<int> colmap, tileE;
+    if (mode == EDM_E_TARGET) {
+        std::vector<int> cnt(ECAP + 2, 0);
+        for (int j = 0; j < N; ++j) cnt[hE[j]]++;
+        std::vector<int> seg(ECAP + 2, 0);
+        int64_t pos = 0;
+        for (int e = 1; e <= ECAP; ++e) {
+            seg[e] = (int)pos;
+            const int nt = (cnt[e] + TILE_J - 1) / TILE_J;
+            for (int t = 0; t < nt; ++t) tileE.push_back(e);
+            pos += (int64_t)nt * TILE_J;
+        }
+        colmap.assign(pos, -1);
+        std::vector<int> fill(seg);
+        for (int j = 0; j < N; ++j) colmap[fill[hE[j]]++] = j;
+    } else {
+        const int nt = (N + TILE_J - 1) / TILE_J;
+        colmap.assign((size_t)nt * TILE_J, -1);
+        for (int j = 0; j < N; ++j) colmap[j] = j;
+        tileE.assign(nt, 0);
+    }
+    const int ntiles = (int)tileE.size();
+    const int Np = ntiles * TILE_J;
+    // library slots
+    const int nlib = lib_end - lib_begin;
+    std::vector<int> sser(nlib), srow(nlib), sE(nlib);
+    for (int r = 0; r < nlib; ++r) { sser[r] = r; srow[r] = r; sE[r] = hE[lib_begin + r]; }
+    CUDA_TRY(cudaMemcpyAsync(W.colmap, colmap.data(), sizeof(int) * Np, cudaMemcpyHostToDevice, cs));
+    CUDA_TRY(cudaMemcpyAsync(W.tileE, tileE.data(), sizeof(int) * ntiles, cudaMemcpyHostToDevice, cs));
+    CUDA_TRY(cudaMemcpyAsync(W.slot_series, sser.data(), sizeof(int) * nlib, cudaMemcpyHostToDevice, cs));
+    CUDA_TRY(cudaMemcpyAsync(W.slot_row, srow.data(), sizeof(int) * nlib, cudaMemcpyHostToDevice, cs));
+    CUDA_TRY(cudaMemcpyAsync(W.slotE, sE.data(), sizeof(int) * nlib, cudaMemcpyHostToDevice, cs));
+
+    // ---- ingest and target preparation (S0, S5)
+    {
+        dim3 tb(32, 8), tg((nlib + 31) / 32, (L + 31) / 32);
+        PROF_LAUNCH(EDM_PROF_PREP, cs, transpose_kernel<<<tg, tb, 0, cs>>>(ds.data, ds.ld, L, lib_begin, nlib, W.Xs));
+        LAUNCH_CHECK("transpose_kernel");
+        PROF_LAUNCH(EDM_PROF_PREP, cs, colprep_kernel<<<(N + 127) / 128, 128, 0, cs>>>(ds.data, ds.ld, N, L, W.mean, W.lastdiff));
+        LAUNCH_CHECK("colprep_kernel");
+        dim3 pg((Np + 255) / 256, std::min(L, 256));
+        PROF_LAUNCH(EDM_PROF_PREP, cs, permute_kernel<<<pg, 256, 0, cs>>>(ds.data, ds.ld, L, Np, W.colmap, W.mean, W.lastdiff, W.Yp, W.lastdiff_p));
+        LAUNCH_CHECK("permute_kernel");
+        PROF_LAUNCH(EDM_PROF_PREP, cs, stats_kernel<<<(Np + 127) / 128, 128, 0, cs>>>(W.Yp, L, Np, tau, Tp, ECAP, W.stats));
+        LAUNCH_CHECK("stats_kernel");
+    }
+
+    // ---- library blocks: kNN tables (S6-S8) then lookup + rho (S9, S10)
+    const size_t tile_smem = (size_t)L * TILE_J * sizeof(float);
+    const bool use_smem = tile_smem <= (size_t)LOOKUP_SMEM_MAX;
+    if (use_smem) CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem));
+    for (int r0 = 0; r0 < nlib; r0 += CCM_B) {
+        const int nb = std::min(CCM_B, nlib - r0);
+        KnnParams P{};
+        P.X = W.Xs; P.ldx = L; P.slot_series = W.slot_series + r0;
+        P.L = L; P.tau = tau; P.Tp = Tp; P.excl = exclude_self ? 1 : 0;
+        P.maskS = maskS; P.Etop = Etop;
+        P.slotE = (mode == EDM_E_LIBRARY) ? W.slotE + r0 : nullptr;
+        P.tables = W.tables; P.T_lib = T_lib;
+        memcpy(P.offE, offE, sizeof(offE));
+        st = launch_knn<MODE_CCM>(P, L - Tp, nb, (size_t)L * sizeof(double), cs);
+        if (st != EDM_OK) return st;
+        LookupParams Q{};
+        Q.Yp = W.Yp; Q.Np = Np; Q.colmap = W.colmap;
+        Q.tileE = (mode == EDM_E_TARGET) ? W.tileE : nullptr;
+        Q.slotE = W.slotE + r0; Q.slotRow = W.slot_row + r0;
+        Q.tables = W.tables; Q.T_lib = T_lib;
+        memcpy(Q.offE, offE, sizeof(offE));
+        Q.stats = W.stats; Q.lastdiff = W.lastdiff_p;
+        Q.L = L; Q.tau = tau; Q.Tp = Tp; Q.B = nb; Q.N = N; Q.rho = rho;
+        if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles, LOOKUP_WARPS * 32, tile_smem, cs>>>(Q));
+        else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles, LOOKUP_WARPS * 32, 0, cs>>>(Q));
+        LAUNCH_CHECK("lookup_kernel");
+    }
+    return EDM_OK;
+}
+
+edm_status edm_causal_map_host(const float* host_data, int32_t N, int32_t L, int32_t E_max, int32_t tau, int32_t Tp,
+                               edm_e_mode mode, int32_t exclude_self, int32_t* host_optE, float* host_rho,
+                               float* host_rhoE) {
+    if (!host_data || !host_rho) return fail(EDM_EINVAL, "null pointer");
+    const size_t ws0 = edm_workspace_bytes(0, N, L, E_max, tau, 1);
+    const size_t ws1 = edm_workspace_bytes(1, N, L, E_max, tau, Tp);
+    if (ws0 == 0 || ws1 == 0) return fail(EDM_EINVAL, "bad arguments N=%d L=%d E_max=%d tau=%d Tp=%d", N, L, E_max, tau, Tp);
+    edm_status st = check_device();
+    if (st != EDM_OK) return st;
+    cudaStream_t cs;
+    CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    float *d_data = nullptr, *d_rho = nullptr, *d_rhoE = nullptr;
+    int32_t* d_E = nullptr;
+    void* ws = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(d_data); cudaFree(d_rho); cudaFree(d_rhoE); cudaFree(d_E); cudaFree(ws);
+        cudaStreamDestroy(cs);
+    };
+    auto run = [&]() -> edm_status {
+        CUDA_TRY(cudaMalloc(&d_data, sizeof(float) * (size_t)N * L));
+        CUDA_TRY(cudaMalloc(&d_rho, sizeof(float) * (size_t)N * N));
+        CUDA_TRY(cudaMalloc(&d_E, sizeof(int32_t) * N));
+        if (host_rhoE) CUDA_TRY(cudaMalloc(&d_rhoE, sizeof(float) * (size_t)N * E_max));
+        CUDA_TRY(cudaMalloc(&ws, std::max(ws0, ws1)));
+        CUDA_TRY(cudaMemcpyAsync(d_data, host_data, sizeof(float) * (size_t)N * L, cudaMemcpyHostToDevice, cs));
+        edm_dataset ds{d_data, N, L, N};
+        edm_status s = edm_simplex_optimal_E(ds, E_max, tau, 0, N, d_E, d_rhoE, ws, std::max(ws0, ws1), cs);
+        if (s != EDM_OK) return s;
+        s = edm_ccm_all_pairs(ds, d_E, tau, Tp, mode, exclude_self, 0, N, d_rho, ws, std::max(ws0, ws1), cs);
+        if (s != EDM_OK) return s;
+        CUDA_TRY(cudaMemcpyAsync(host_rho, d_rho, sizeof(float) * (size_t)N * N, cudaMemcpyDeviceToHost, cs));
+        if (host_optE) CUDA_TRY(cudaMemcpyAsync(host_optE, d_E, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, cs));
+        if (host_rhoE) CUDA_TRY(cudaMemcpyAsync(host_rhoE, d_rhoE, sizeof(float) * (size_t)N * E_max, cudaMemcpyDeviceToHost, cs));
+        CUDA_TRY(cudaStreamSynchronize(cs));
+        return EDM_OK;
+    };
+    st = run();
+    cleanup();
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,216 @@
+"""Thin Python binding of libccm (include/libccm.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of libccm.so; this module converts
+torch tensors to device pointers, passes torch's current CUDA stream, owns the workspace
+and raises on a non-OK status. There is no CPU fallback: if libccm.so is missing or the
+device is not a B200 the calls raise.
+
+Names follow the C ABI (PAPER.md problem statement P:316-317):
+  embed_knn(series, E, tau, Tp)              -> idx, dist, w          (edm_embed_knn)
+  simplex_optimal_E(data, E_max, tau)        -> optE[, rhoE]          (edm_simplex_optimal_E)
+  ccm_all_pairs(data, E, tau, Tp, mode)      -> rho rows              (edm_ccm_all_pairs)
+  causal_map_host(host array, ...)           -> optE, rho (numpy)     (edm_causal_map_host)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import build as _build
+
+EDM_OK, EDM_EINVAL, EDM_ETOOSHORT, EDM_EWORKSPACE, EDM_ECUDA, EDM_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
+EDM_E_TARGET, EDM_E_LIBRARY = 0, 1
+E_CAP = 20
+
+EXPORTS = ("edm_embed_knn", "edm_simplex_optimal_E", "edm_ccm_all_pairs", "edm_workspace_bytes",
+           "edm_causal_map_host", "edm_last_error", "edm_version", "edm_profile_begin", "edm_profile_end")
+PROF_KINDS = ("prep", "simplex_knn", "simplex_rho", "ccm_knn", "lookup", "other")
+
+
+class EdmError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"libccm status {status}: {msg}")
+        self.status = status
+
+
+class edm_dataset(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("N", C.c_int32), ("L", C.c_int32), ("ld", C.c_int64)]
+
+
+_lib = None
+
+
+def load(path: Optional[str] = None):
+    """Load libccm.so (built in-tree by build.py). Raises if it is missing: no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or _build.LIB
+    if not os.path.exists(path):
+        raise ImportError(f"libccm.so not found at {path}; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(path)
+    i32, vp, sz = C.c_int32, C.c_void_p, C.c_size_t
+    lib.edm_embed_knn.restype = i32
+    lib.edm_embed_knn.argtypes = [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp]
+    lib.edm_simplex_optimal_E.restype = i32
+    lib.edm_simplex_optimal_E.argtypes = [edm_dataset, i32, i32, i32, i32, vp, vp, vp, sz, vp]
+    lib.edm_ccm_all_pairs.restype = i32
+    lib.edm_ccm_all_pairs.argtypes = [edm_dataset, vp, i32, i32, i32, i32, i32, i32, vp, vp, sz, vp]
+    lib.edm_workspace_bytes.restype = sz
+    lib.edm_workspace_bytes.argtypes = [i32, i32, i32, i32, i32, i32]
+    lib.edm_causal_map_host.restype = i32
+    lib.edm_causal_map_host.argtypes = [vp, i32, i32, i32, i32, i32, i32, i32, vp, vp, vp]
+    lib.edm_last_error.restype = C.c_char_p
+    lib.edm_last_error.argtypes = []
+    lib.edm_version.restype = C.c_char_p
+    lib.edm_version.argtypes = []
+    lib.edm_profile_begin.restype = i32
+    lib.edm_profile_begin.argtypes = []
+    lib.edm_profile_end.restype = i32
+    lib.edm_profile_end.argtypes = [vp, vp]
+    _lib = lib
+    return lib
+
+
+def _check(status: int):
+    if status != EDM_OK:
+        raise EdmError(status, load().edm_last_error().decode())
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _require_cuda(t: torch.Tensor, dtype, name):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (libccm has no CPU path)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+
+
+def _dataset(data: torch.Tensor) -> edm_dataset:
+    _require_cuda(data, torch.float32, "data")
+    if data.dim() != 2 or data.stride(1) != 1:
+        raise ValueError("data must be a [L, N] time-major tensor with unit column stride")
+    L, N = data.shape
+    return edm_dataset(data.data_ptr(), N, L, data.stride(0))
+
+
+_ws_cache: dict = {}
+
+
+def workspace(which: int, N: int, L: int, E_max: int, tau: int, Tp: int, device) -> torch.Tensor:
+    nbytes = load().edm_workspace_bytes(which, N, L, E_max, tau, Tp)
+    if nbytes == 0:
+        raise EdmError(EDM_EINVAL, f"bad workspace request which={which} N={N} L={L} E_max={E_max}")
+    key = (which, torch.device(device))
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() < nbytes:
+        _ws_cache.pop(key, None)
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def release_workspaces():
+    _ws_cache.clear()
+
+
+def embed_knn(series: torch.Tensor, E: int, tau: int = 1, Tp: int = 1, exclude_self: bool = True,
+              with_weights: bool = True):
+    """kNN table of one series at E (phase-2 form): idx int32 [n_E, E+1], dist fp32, w fp32."""
+    _require_cuda(series, torch.float32, "series")
+    series = series.contiguous()
+    L = series.numel()
+    n = max(L - (E - 1) * tau - Tp, 1)
+    idx = torch.empty((n, E + 1), dtype=torch.int32, device=series.device)
+    dist = torch.empty((n, E + 1), dtype=torch.float32, device=series.device)
+    w = torch.empty((n, E + 1), dtype=torch.float32, device=series.device) if with_weights else None
+    _check(load().edm_embed_knn(series.data_ptr(), L, E, tau, Tp, int(exclude_self), idx.data_ptr(),
+                                dist.data_ptr(), w.data_ptr() if w is not None else None, _stream(series.device)))
+    return idx, dist, w
+
+
+def simplex_optimal_E(data: torch.Tensor, E_max: int = 20, tau: int = 1, s_begin: int = 0,
+                      s_end: Optional[int] = None, return_rho: bool = False):
+    """Phase 1: optimal E of series [s_begin, s_end) -> int32 tensor (and rhoE [n, E_max])."""
+    ds = _dataset(data)
+    s_end = ds.N if s_end is None else s_end
+    n = s_end - s_begin
+    optE = torch.empty(max(n, 0), dtype=torch.int32, device=data.device)
+    rhoE = torch.empty((max(n, 0), E_max), dtype=torch.float32, device=data.device) if return_rho else None
+    ws = workspace(0, ds.N, ds.L, E_max, tau, 1, data.device)
+    _check(load().edm_simplex_optimal_E(ds, E_max, tau, s_begin, s_end, optE.data_ptr(),
+                                        rhoE.data_ptr() if rhoE is not None else None, ws.data_ptr(), ws.numel(),
+                                        _stream(data.device)))
+    return (optE, rhoE) if return_rho else optE
+
+
+def _mode(mode) -> int:
+    if mode in ("target", EDM_E_TARGET):
+        return EDM_E_TARGET
+    if mode in ("library", EDM_E_LIBRARY):
+        return EDM_E_LIBRARY
+    raise ValueError(f"mode must be 'target' or 'library', got {mode!r}")
+
+
+def ccm_all_pairs(data: torch.Tensor, E: torch.Tensor, tau: int = 1, Tp: int = 1, mode="target",
+                  exclude_self: bool = True, lib_begin: int = 0, lib_end: Optional[int] = None,
+                  out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Phase 2: rho[i - lib_begin, j] for library rows [lib_begin, lib_end) and all targets j."""
+    ds = _dataset(data)
+    _require_cuda(E, torch.int32, "E")
+    E = E.contiguous()
+    if E.numel() != ds.N:
+        raise ValueError("E must have N entries")
+    lib_end = ds.N if lib_end is None else lib_end
+    rows = lib_end - lib_begin
+    if out is None:
+        out = torch.empty((max(rows, 0), ds.N), dtype=torch.float32, device=data.device)
+    else:
+        _require_cuda(out, torch.float32, "out")
+        if not out.is_contiguous() or out.numel() < rows * ds.N:
+            raise ValueError("out must be contiguous with at least rows*N elements")
+    ws = workspace(1, ds.N, ds.L, E_CAP, tau, Tp, data.device)
+    _check(load().edm_ccm_all_pairs(ds, E.data_ptr(), tau, Tp, _mode(mode), int(exclude_self), lib_begin, lib_end,
+                                    out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(data.device)))
+    return out
+
+
+def causal_map(data: torch.Tensor, E_max: int = 20, tau: int = 1, Tp: int = 1, mode="target",
+               exclude_self: bool = True):
+    """Both phases on one GPU from a device-resident dataset -> (optE, rho [N, N])."""
+    optE = simplex_optimal_E(data, E_max, tau)
+    rho = ccm_all_pairs(data, optE, tau, Tp, mode, exclude_self)
+    return optE, rho
+
+
+def causal_map_host(data: np.ndarray, E_max: int = 20, tau: int = 1, Tp: int = 1, mode="target",
+                    exclude_self: bool = True, rho_out: Optional[np.ndarray] = None, with_rhoE: bool = False):
+    """End-to-end from host memory through edm_causal_map_host (H2D, both phases, D2H)."""
+    data = np.ascontiguousarray(data, dtype=np.float32)
+    L, N = data.shape
+    optE = np.empty(N, np.int32)
+    rho = rho_out if rho_out is not None else np.empty((N, N), np.float32)
+    assert rho.dtype == np.float32 and rho.flags.c_contiguous and rho.size >= N * N
+    rhoE = np.empty((N, E_max), np.float32) if with_rhoE else None
+    _check(load().edm_causal_map_host(data.ctypes.data, N, L, E_max, tau, Tp, _mode(mode), int(exclude_self),
+                                      optE.ctypes.data, rho.ctypes.data, rhoE.ctypes.data if with_rhoE else None))
+    return (optE, rho, rhoE) if with_rhoE else (optE, rho)
+
+
+def profile_begin():
+    """Start bracketing every libccm launch on this thread with CUDA events (bench.py)."""
+    _check(load().edm_profile_begin())
+
+
+def profile_end():
+    """Stop profiling -> {kind: (device ms summed over launches, launch count)}."""
+    ms = (C.c_double * len(PROF_KINDS))()
+    n = (C.c_int64 * len(PROF_KINDS))()
+    _check(load().edm_profile_end(ms, n))
+    return {k: (ms[i], n[i]) for i, k in enumerate(PROF_KINDS)}
