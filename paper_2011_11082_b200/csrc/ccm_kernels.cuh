@@ -20,8 +20,9 @@ namespace ccm {
 
 constexpr int ECAP = 20;            // largest E (k = E + 1 <= 21 <= 32 lanes)
 constexpr int TILE_J = 32;          // targets per lookup tile (one per lane)
-constexpr int KNN_WARPS = 8;        // warps per knn CTA
-constexpr int KNN_QPW = 8;          // queries per warp per CTA
+constexpr int KNN_WARPS = 4;        // warps per knn CTA
+constexpr int KNN_MIN_CTAS = 3;     // resident CTAs per SM the register budget must allow
+constexpr int KNN_QPW = 16;         // consecutive queries per warp
 constexpr int KNN_QPB = KNN_WARPS * KNN_QPW;
 constexpr int LOOKUP_WARPS = 16;    // warps per lookup CTA (one library each)
 constexpr unsigned FULL = 0xffffffffu;
@@ -129,7 +130,9 @@ __device__ __forceinline__ int hi_word(double d) { return __double2hiint(d); }
 // Insert every lane flagged in `bal` into the warp-distributed sorted list (lane j holds
 // entry j, lanes >= k hold +inf). Candidates arrive in increasing s (lanes low -> high,
 // chunks in order), so an entry already in the list with an equal distance has a smaller
-// index and stays in front: the (d2, s) lexicographic order of C4 / S:137.
+// index and stays in front: the (d2, s) lexicographic order of C4 / S:137. A candidate whose
+// position would be >= k is rejected. thr (hi word of the k-th entry, used as a cheap
+// prefilter) only ever decreases: it may start at a seeded bound (knn_warp).
 __device__ __forceinline__ void list_insert(unsigned bal, double D, int s, int k, int lane,
                                             double& Ld, int& Ls, int& thr) {
     while (bal) {
@@ -137,15 +140,14 @@ __device__ __forceinline__ void list_insert(unsigned bal, double D, int s, int k
         bal &= bal - 1;
         const double Dn = __shfl_sync(FULL, D, src);
         const int sn = __shfl_sync(FULL, s, src);
-        const double th = __shfl_sync(FULL, Ld, k - 1);
-        if (Dn < th) {
-            const int pos = __popc(__ballot_sync(FULL, Ld <= Dn));
-            const double ud = __shfl_up_sync(FULL, Ld, 1);
-            const int us = __shfl_up_sync(FULL, Ls, 1);
+        const double ud = __shfl_up_sync(FULL, Ld, 1);
+        const int us = __shfl_up_sync(FULL, Ls, 1);
+        const int pos = __popc(__ballot_sync(FULL, Ld <= Dn));
+        if (pos < k) {
             if (lane > pos) { Ld = ud; Ls = us; }
             if (lane == pos) { Ld = Dn; Ls = sn; }
             if (lane >= k) { Ld = CUDART_INF; Ls = 0x7fffffff; }
-            thr = hi_word(__shfl_sync(FULL, Ld, k - 1));
+            thr = min(thr, hi_word(__shfl_sync(FULL, Ld, k - 1)));
         }
     }
 }
@@ -173,82 +175,120 @@ __device__ __forceinline__ double simplex_weight(double d2, int k, int lane) {
     return __ddiv_rn(u, sum);
 }
 
-// One query point t (one warp): D_E(t, s) for E = 1..Eq accumulated incrementally over E
-// (D_E = D_{E-1} + (a[t-(E-1)tau] - b[s-(E-1)tau])^2, the same fp64 operation sequence as
-// the oracle's C3 loop, so every D_E is bit-identical to the oracle's), and at every E in the
-// selected set a top-(E+1) list by (D_E, s).
+// One warp, queries t = t_begin .. t_end-1 in order. For each query: D_E(t, s) for E = 1..Eq
+// accumulated incrementally over E (D_E = D_{E-1} + (a[t-(E-1)tau] - b[s-(E-1)tau])^2, the
+// same fp64 operation sequence as the oracle's C3 loop, so every D_E is bit-identical to the
+// oracle's) and, at every E in the selected set, a top-(E+1) list by (D_E, s).
+//
+// Seeded thresholds (E >= 3): the successors s+1 of query t-1's neighbours at the same E
+// are usually near neighbours of t (the dynamics carries neighbourhoods along). Their exact
+// distances D_E(t, s+1) give k distinct evaluated candidates, so their maximum is an upper
+// bound on the k-th smallest distance; candidates above it can never enter the list and
+// are filtered before the insertion path. This changes the work, not the result.
 template <int MODE>
-__device__ __forceinline__ void knn_query(const KnnParams& P, const double* __restrict__ qa,
-                                          const double* __restrict__ cb, int t, int ncand,
-                                          unsigned mask, int Etop, int b, int lane) {
+__device__ __forceinline__ void knn_warp(const KnnParams& P, const double* __restrict__ qa,
+                                         const double* __restrict__ cb, int t_begin, int t_end, int ncand,
+                                         unsigned mask, int Etop, int b, int lane) {
     const int tau = P.tau;
-    const int Eq = min(Etop, t / tau + 1);  // E with (E-1) tau <= t
     const bool excl = (MODE != MODE_SIMPLEX) && P.excl;
-    double q[ECAP];
     double Ld[ECAP];
     int Ls[ECAP], thr[ECAP];
 #pragma unroll
-    for (int e = 0; e < ECAP; ++e) {
-        q[e] = (e < Eq) ? qa[t - e * tau] : 0.0;
-        Ld[e] = CUDART_INF;
-        Ls[e] = 0x7fffffff;
-        thr[e] = 0x7ff00000;  // hi word of +inf
-    }
-    for (int c0 = 0; c0 < ncand; c0 += 32) {
-        const int s = c0 + lane;
-        const bool valid = (s < ncand) && !(excl && s == t);
-        double D = 0.0;
+    for (int e = 0; e < ECAP; ++e) { Ld[e] = CUDART_INF; Ls[e] = 0x7fffffff; }
+    int prevEq = 0;  // lists hold the final neighbours of query t-1 for E <= prevEq
+    for (int t = t_begin; t < t_end; ++t) {
+        const int Eq = min(Etop, t / tau + 1);  // E with (E-1) tau <= t
+        double q[ECAP];
+#pragma unroll
+        for (int e = 0; e < ECAP; ++e) q[e] = (e < Eq) ? qa[t - e * tau] : 0.0;
+        // ---- seeded thresholds from the previous query's lists, then reset the lists
 #pragma unroll
         for (int e = 0; e < ECAP; ++e) {
-            if (e < Eq) {
-                const int sm = s - e * tau;
-                const bool ve = valid && sm >= 0;
-                const double xv = cb[max(min(sm, ncand - 1), 0)];
-                const double diff = __dsub_rn(q[e], xv);
-                D = __dadd_rn(D, __dmul_rn(diff, diff));
-                if ((mask >> (e + 1)) & 1u) {
-                    // prefilter on the high word: D < theta implies hi(D) <= hi(theta) (D >= 0)
-                    const unsigned bal = __ballot_sync(FULL, ve && hi_word(D) <= thr[e]);
-                    if (bal) list_insert(bal, D, s, e + 2, lane, Ld[e], Ls[e], thr[e]);
-                }
-            }
-        }
-    }
-    // finalise every selected E of this query
+            thr[e] = 0x7ff00000;  // hi word of +inf
+            if (e >= 2 && e < Eq && e < prevEq && ((mask >> (e + 1)) & 1u)) {
+                const int k = e + 2;
+                const int c = Ls[e] + 1;
+                const bool ok = lane < k && c < ncand && c - e * tau >= 0 && !(excl && c == t);
+                double D = CUDART_INF;
+                if (ok) {
+                    D = 0.0;
 #pragma unroll
-    for (int e = 0; e < ECAP; ++e) {
-        if (e < Eq && ((mask >> (e + 1)) & 1u)) {
-            const int k = e + 2;
-            const int row = t - e * tau;
-            if (MODE == MODE_CCM) {
-                const double w = simplex_weight<false>(Ld[e], k, lane);
-                const int kp = kpad(k);
-                if (lane < kp) {
-                    uint2 ent = lane < k ? make_uint2((unsigned)(Ls[e] + P.Tp), __float_as_uint((float)w))
-                                         : make_uint2(0u, 0u);
-                    P.tables[(int64_t)b * P.T_lib + P.offE[e + 1] + (int64_t)row * kp + lane] = ent;
+                    for (int m = 0; m <= e; ++m) {
+                        const double diff = __dsub_rn(q[m], cb[c - m * tau]);
+                        D = __dadd_rn(D, __dmul_rn(diff, diff));
+                    }
                 }
-            } else if (MODE == MODE_EMBED) {
-                const double w = simplex_weight<true>(Ld[e], k, lane);
-                if (lane < k) {
-                    P.out_idx[(int64_t)row * k + lane] = Ls[e];
-                    P.out_dist[(int64_t)row * k + lane] = (float)sqrt(Ld[e]);
-                    if (P.out_w) P.out_w[(int64_t)row * k + lane] = (float)w;
+                const unsigned okb = __ballot_sync(FULL, ok);
+                if (okb == ((1u << k) - 1u)) {
+                    double th = lane < k ? D : 0.0;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) th = fmax(th, __shfl_xor_sync(FULL, th, o));
+                    thr[e] = hi_word(th);
                 }
-            } else {  // MODE_SIMPLEX: forecast one step ahead, yhat = sum_k w_k lib[s_k + 1]
-                const double w = simplex_weight<true>(Ld[e], k, lane);
-                const double prod = lane < k ? __dmul_rn(w, cb[Ls[e] + 1]) : 0.0;
-                double acc = 0.0;
-                for (int j = 0; j < k; ++j) acc = __dadd_rn(acc, __shfl_sync(FULL, prod, j));
-                if (lane == 0) P.pred[((int64_t)b * ECAP + e) * P.LQ + t] = acc;
+            }
+            Ld[e] = CUDART_INF;
+            Ls[e] = 0x7fffffff;
+        }
+        // ---- sweep over the candidates in increasing s
+        for (int c0 = 0; c0 < ncand; c0 += 32) {
+            const int s = c0 + lane;
+            const bool valid = (s < ncand) && !(excl && s == t);
+            double D = 0.0;
+#pragma unroll
+            for (int e = 0; e < ECAP; ++e) {
+                if (e < Eq) {
+                    const int sm = s - e * tau;
+                    const bool ve = valid && sm >= 0;
+                    const double xv = cb[max(min(sm, ncand - 1), 0)];
+                    const double diff = __dsub_rn(q[e], xv);
+                    D = __dadd_rn(D, __dmul_rn(diff, diff));
+                    if ((mask >> (e + 1)) & 1u) {
+                        // prefilter on the high word: D <= theta implies hi(D) <= hi(theta) (D >= 0)
+                        const unsigned bal = __ballot_sync(FULL, ve && hi_word(D) <= thr[e]);
+                        if (bal) list_insert(bal, D, s, e + 2, lane, Ld[e], Ls[e], thr[e]);
+                    }
+                }
             }
         }
+        // ---- finalise every selected E of this query
+#pragma unroll
+        for (int e = 0; e < ECAP; ++e) {
+            if (e < Eq && ((mask >> (e + 1)) & 1u)) {
+                const int k = e + 2;
+                const int row = t - e * tau;
+                if (MODE == MODE_CCM) {
+                    const double w = simplex_weight<false>(Ld[e], k, lane);
+                    const int kp = kpad(k);
+                    if (lane < kp) {
+                        uint2 ent = lane < k ? make_uint2((unsigned)(Ls[e] + P.Tp), __float_as_uint((float)w))
+                                             : make_uint2(0u, 0u);
+                        P.tables[(int64_t)b * P.T_lib + P.offE[e + 1] + (int64_t)row * kp + lane] = ent;
+                    }
+                } else if (MODE == MODE_EMBED) {
+                    const double w = simplex_weight<true>(Ld[e], k, lane);
+                    if (lane < k) {
+                        P.out_idx[(int64_t)row * k + lane] = Ls[e];
+                        P.out_dist[(int64_t)row * k + lane] = (float)sqrt(Ld[e]);
+                        if (P.out_w) P.out_w[(int64_t)row * k + lane] = (float)w;
+                    }
+                } else {  // MODE_SIMPLEX: forecast one step ahead, yhat = sum_k w_k lib[s_k + 1]
+                    const double w = simplex_weight<true>(Ld[e], k, lane);
+                    const double prod = lane < k ? __dmul_rn(w, cb[Ls[e] + 1]) : 0.0;
+                    double acc = 0.0;
+                    for (int j = 0; j < k; ++j) acc = __dadd_rn(acc, __shfl_sync(FULL, prod, j));
+                    if (lane == 0) P.pred[((int64_t)b * ECAP + e) * P.LQ + t] = acc;
+                }
+            }
+        }
+        prevEq = Eq;
     }
 }
 
 // grid = (ceil(nq / KNN_QPB), slots); block = KNN_WARPS * 32; dynamic smem = L doubles.
+// Warp w of CTA x handles the contiguous queries [x*QPB + w*QPW, +QPW) (so that each query
+// can seed its thresholds from the previous one).
 template <int MODE>
-__global__ void __launch_bounds__(KNN_WARPS * 32) knn_kernel(KnnParams P) {
+__global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnParams P) {
     extern __shared__ double xs[];
     const int b = blockIdx.y;
     const int row = P.slot_series ? P.slot_series[b] : b;
@@ -276,9 +316,9 @@ __global__ void __launch_bounds__(KNN_WARPS * 32) knn_kernel(KnnParams P) {
         nq = ncand = P.L - P.Tp;          // P_1 = [0, L-1-Tp]; per-E lower bound (E-1)tau
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int t_end = min(nq, (int)(blockIdx.x + 1) * KNN_QPB);
-    for (int t = blockIdx.x * KNN_QPB + warp; t < t_end; t += KNN_WARPS)
-        knn_query<MODE>(P, qa, cb, t, ncand, mask, Etop, b, lane);
+    const int t0 = blockIdx.x * KNN_QPB + warp * KNN_QPW;
+    const int t1 = min(nq, t0 + KNN_QPW);
+    if (t0 < t1) knn_warp<MODE>(P, qa, cb, t0, t1, ncand, mask, Etop, b, lane);
 }
 
 // ------------------------------------------------------------------ S2 / S3 phase-1 skill
@@ -351,40 +391,95 @@ struct LookupParams {
     float* rho;
 };
 
+// ---- per-warp table staging: TMA bulk copies (cp.async.bulk) into a 2-stage shared-memory
+// ring, completion tracked by an mbarrier per stage (expect_tx / complete_tx).
+constexpr int LK_CHUNK = 1024;  // bytes per stage
+constexpr int LK_STAGES = 2;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// one elected lane: arm the barrier with the byte count and launch the bulk copy
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+struct WarpRing {
+    uint4* buf;      // LK_STAGES * LK_CHUNK bytes
+    uint64_t* bar;   // LK_STAGES mbarriers
+    uint32_t it;     // chunks consumed so far by this warp (stage = it % 2, parity = (it / 2) & 1)
+};
+
 // p(t) = sum_j w_j y[s_j + Tp] (Alg. 5) for the lane's target over the rows of
 // one table, with the Pearson moments sum p, sum p^2, sum p*o accumulated on the fly (fp32
-// within 32-row blocks, fp64 across blocks); o = y[t + Tp]. Then rho from the moments and the
-// precomputed fp64 sums of o (C10).
-template <int E, bool SMEM>
+// within chunks, fp64 across chunks); o = y[t + Tp]. Then rho from the moments and the
+// precomputed fp64 sums of o (C10). Table rows stream through the warp's TMA ring;
+// every (idx, w) pair is a warp-uniform shared-memory broadcast, every y a conflict-free
+// lane-contiguous shared-memory read of the staged target tile.
+template <int E>
 __device__ __forceinline__ void lookup_one(const LookupParams& P, const float* __restrict__ Y, int64_t ys,
-                                           int tile, int b, int lane, int col) {
+                                           int tile, int b, int lane, int col, WarpRing& R) {
     constexpr int k = E + 1, kp = kpad(k);
-    const uint4* tab = reinterpret_cast<const uint4*>(P.tables + (int64_t)b * P.T_lib + P.offE[E]);
+    constexpr int ROWS = LK_CHUNK / (8 * kp);       // whole rows per chunk
+    constexpr int CB = ROWS * kp * 8;               // bytes of a full chunk (multiple of 16)
+    const char* tab = reinterpret_cast<const char*>(P.tables + (int64_t)b * P.T_lib + P.offE[E]);
     const int t0 = (E - 1) * P.tau;
     const int n = P.L - t0 - P.Tp;
+    const int nch = (n + ROWS - 1) / ROWS;
+    auto issue = [&](int ci, uint32_t slot) {
+        const int rows = min(ROWS, n - ci * ROWS);
+        tma_load_1d(R.buf + slot * (LK_CHUNK / 16), tab + (int64_t)ci * CB, (uint32_t)(rows * kp * 8), R.bar + slot);
+    };
+    if (lane == 0) {
+        fence_proxy_async();  // earlier generic reads of the ring before the async-proxy writes
+        issue(0, R.it % LK_STAGES);
+        if (nch > 1) issue(1, (R.it + 1) % LK_STAGES);
+    }
     double Sp = 0.0, Spp = 0.0, Spo = 0.0;
     const float* Yo = Y + (int64_t)(t0 + P.Tp) * ys + lane;
     const float* Yl = Y + lane;
-    auto predict = [&](int r) {
-        const uint4* row = tab + (int64_t)r * (kp / 2);
-        float p = 0.f;
-#pragma unroll
-        for (int j2 = 0; j2 < kp / 2; ++j2) {
-            const uint4 e2 = __ldg(row + j2);
-            p = fmaf(__uint_as_float(e2.y), Yl[(int64_t)e2.x * ys], p);
-            if (2 * j2 + 1 < k) p = fmaf(__uint_as_float(e2.w), Yl[(int64_t)e2.z * ys], p);
-        }
-        return p;
-    };
-    // moments of the prediction shifted by its first value: no cancellation when the
-    // prediction is (nearly) constant, e.g. a constant library series (all neighbours tie)
-    const float c = predict(0);
-    for (int r0 = 0; r0 < n; r0 += 32) {
-        const int r1 = min(n, r0 + 32);
+    float c = 0.f;  // shift: the first prediction (no cancellation for near-constant predictions)
+    for (int ci = 0; ci < nch; ++ci) {
+        const uint32_t slot = R.it % LK_STAGES;
+        mbar_wait(R.bar + slot, (R.it / LK_STAGES) & 1u);
+        const uint4* rowp = R.buf + slot * (LK_CHUNK / 16);
+        const int r0 = ci * ROWS, r1 = min(n, r0 + ROWS);
         float sp = 0.f, spp = 0.f, spo = 0.f;
 #pragma unroll 2
         for (int r = r0; r < r1; ++r) {
-            const float p = predict(r) - c;
+            const uint4* row = rowp + (r - r0) * (kp / 2);
+            float p = 0.f;
+#pragma unroll
+            for (int j2 = 0; j2 < kp / 2; ++j2) {
+                const uint4 e2 = row[j2];
+                p = fmaf(__uint_as_float(e2.y), Yl[(int64_t)e2.x * ys], p);
+                if (2 * j2 + 1 < k) p = fmaf(__uint_as_float(e2.w), Yl[(int64_t)e2.z * ys], p);
+            }
+            if (r == 0) c = p;
+            p -= c;
             const float o = Yo[(int64_t)r * ys];
             sp += p;
             spp = fmaf(p, p, spp);
@@ -393,6 +488,12 @@ __device__ __forceinline__ void lookup_one(const LookupParams& P, const float* _
         Sp += (double)sp;
         Spp += (double)spp;
         Spo += (double)spo;
+        __syncwarp();  // every lane is done reading this stage
+        ++R.it;
+        if (lane == 0 && ci + 2 < nch) {
+            fence_proxy_async();
+            issue(ci + 2, slot);
+        }
     }
     if (col >= 0) {
         const int pcol = tile * TILE_J + lane;
@@ -408,11 +509,10 @@ __device__ __forceinline__ void lookup_one(const LookupParams& P, const float* _
     }
 }
 
-template <bool SMEM>
 __device__ __forceinline__ void lookup_dispatch(int E, const LookupParams& P, const float* Y, int64_t ys, int tile,
-                                                int b, int lane, int col) {
+                                                int b, int lane, int col, WarpRing& R) {
     switch (E) {
-#define CCM_CASE(e) case e: lookup_one<e, SMEM>(P, Y, ys, tile, b, lane, col); break;
+#define CCM_CASE(e) case e: lookup_one<e>(P, Y, ys, tile, b, lane, col, R); break;
         CCM_CASE(1) CCM_CASE(2) CCM_CASE(3) CCM_CASE(4) CCM_CASE(5) CCM_CASE(6) CCM_CASE(7)
         CCM_CASE(8) CCM_CASE(9) CCM_CASE(10) CCM_CASE(11) CCM_CASE(12) CCM_CASE(13) CCM_CASE(14)
         CCM_CASE(15) CCM_CASE(16) CCM_CASE(17) CCM_CASE(18) CCM_CASE(19) CCM_CASE(20)
@@ -421,17 +521,30 @@ __device__ __forceinline__ void lookup_dispatch(int E, const LookupParams& P, co
     }
 }
 
+constexpr size_t lookup_ring_bytes() { return (size_t)LOOKUP_WARPS * LK_STAGES * (LK_CHUNK + 8); }
+
 // grid = ntiles; block = LOOKUP_WARPS * 32. SMEM = true: the 32-column target tile
 // Yp[0..L)[tile*32 .. +32) is staged in shared memory ([L][32] fp32) once and reused by
 // every library of the block (the table reuse of Alg. 2, turned into target-tile
-// reuse); SMEM = false (long series): gathers straight from L2/HBM.
+// reuse); SMEM = false (long series): gathers straight from L2/HBM. Tiles run in reverse
+// order so that the expensive high-E tiles (target mode) start first.
+// Dynamic smem: [tile: L*32 floats if SMEM][ring: LOOKUP_WARPS*2*LK_CHUNK][bars].
 template <bool SMEM>
 __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupParams P) {
-    extern __shared__ float ytile[];
-    const int tile = blockIdx.x;
+    extern __shared__ __align__(16) unsigned char lk_smem[];
+    const int tile = gridDim.x - 1 - blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int Et = P.tileE ? P.tileE[tile] : 0;
     if (P.tileE && Et <= 0) return;
+    float* ytile = reinterpret_cast<float*>(lk_smem);
+    const size_t tile_bytes = SMEM ? (size_t)P.L * TILE_J * sizeof(float) : 0;
+    uint4* ring = reinterpret_cast<uint4*>(lk_smem + tile_bytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(lk_smem + tile_bytes + (size_t)LOOKUP_WARPS * LK_STAGES * LK_CHUNK);
+    WarpRing R{ring + (size_t)warp * LK_STAGES * (LK_CHUNK / 16), bars + warp * LK_STAGES, 0u};
+    if (lane == 0) {
+        for (int s = 0; s < LK_STAGES; ++s) mbar_init(R.bar + s, 1);
+        fence_mbar_init();
+    }
     const float* Y;
     int64_t ys;
     if (SMEM) {
@@ -441,17 +554,17 @@ __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupPara
             *reinterpret_cast<float4*>(ytile + t * TILE_J + c) =
                 __ldg(reinterpret_cast<const float4*>(src + (int64_t)t * P.Np + c));
         }
-        __syncthreads();
         Y = ytile;
         ys = TILE_J;
     } else {
         Y = P.Yp + (int64_t)tile * TILE_J;
         ys = P.Np;
     }
+    __syncthreads();
     const int col = P.colmap[tile * TILE_J + lane];
     for (int b = warp; b < P.B; b += LOOKUP_WARPS) {
         const int E = P.tileE ? Et : P.slotE[b];
-        lookup_dispatch<SMEM>(E, P, Y, ys, tile, b, lane, col);
+        lookup_dispatch(E, P, Y, ys, tile, b, lane, col, R);
     }
 }
 

@@ -100,7 +100,7 @@ void table_layout(int L, int tau, int Tp, int64_t offE[ECAP + 2], int64_t* T_lib
 }
 
 constexpr int SIMPLEX_SLOTS = 2048;   // series per phase-1 block
-constexpr int CCM_B = LOOKUP_WARPS;   // libraries per phase-2 block (one lookup warp each)
+constexpr int CCM_B = 4 * LOOKUP_WARPS;   // libraries per phase-2 block (4 per lookup warp)
 constexpr int LOOKUP_SMEM_MAX = 227 * 1024;
 
 inline int64_t np_max(int N) { return (int64_t)(N + TILE_J - 1) / TILE_J * TILE_J + (int64_t)TILE_J * ECAP; }
@@ -369,8 +369,10 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int3
 
     // ---- library blocks: kNN tables (S6-S8) then lookup + rho (S9, S10)
     const size_t tile_smem = (size_t)L * TILE_J * sizeof(float);
-    const bool use_smem = tile_smem <= (size_t)LOOKUP_SMEM_MAX;
-    if (use_smem) CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem));
+    const bool use_smem = tile_smem + lookup_ring_bytes() <= (size_t)LOOKUP_SMEM_MAX;
+    const size_t lk_smem = (use_smem ? tile_smem : 0) + lookup_ring_bytes();
+    if (use_smem) CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
+    else CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
     for (int r0 = 0; r0 < nlib; r0 += CCM_B) {
         const int nb = std::min(CCM_B, nlib - r0);
         KnnParams P{};
@@ -390,8 +392,8 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int3
         memcpy(Q.offE, offE, sizeof(offE));
         Q.stats = W.stats; Q.lastdiff = W.lastdiff_p;
         Q.L = L; Q.tau = tau; Q.Tp = Tp; Q.B = nb; Q.N = N; Q.rho = rho;
-        if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles, LOOKUP_WARPS * 32, tile_smem, cs>>>(Q));
-        else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles, LOOKUP_WARPS * 32, 0, cs>>>(Q));
+        if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+        else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
         LAUNCH_CHECK("lookup_kernel");
     }
     return EDM_OK;
