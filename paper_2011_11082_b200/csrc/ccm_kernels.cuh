@@ -21,7 +21,7 @@ namespace ccm {
 constexpr int ECAP = 20;            // largest E (k = E + 1 <= 21 <= 32 lanes)
 constexpr int TILE_J = 32;          // targets per lookup tile (one per lane)
 constexpr int KNN_WARPS = 4;        // warps per knn CTA
-constexpr int KNN_MIN_CTAS = 3;     // resident CTAs per SM the register budget must allow
+constexpr int KNN_MIN_CTAS = 4;     // resident CTAs per SM the register budget must allow
 constexpr int KNN_QPW = 16;         // consecutive queries per warp
 constexpr int KNN_QPB = KNN_WARPS * KNN_QPW;
 constexpr int LOOKUP_WARPS = 16;    // warps per lookup CTA (one library each)
@@ -127,31 +127,6 @@ struct KnnParams {
 
 __device__ __forceinline__ int hi_word(double d) { return __double2hiint(d); }
 
-// Insert every lane flagged in `bal` into the warp-distributed sorted list (lane j holds
-// entry j, lanes >= k hold +inf). Candidates arrive in increasing s (lanes low -> high,
-// chunks in order), so an entry already in the list with an equal distance has a smaller
-// index and stays in front: the (d2, s) lexicographic order of C4 / S:137. A candidate whose
-// position would be >= k is rejected. thr (hi word of the k-th entry, used as a cheap
-// prefilter) only ever decreases: it may start at a seeded bound (knn_warp).
-__device__ __forceinline__ void list_insert(unsigned bal, double D, int s, int k, int lane,
-                                            double& Ld, int& Ls, int& thr) {
-    while (bal) {
-        const int src = __ffs(bal) - 1;
-        bal &= bal - 1;
-        const double Dn = __shfl_sync(FULL, D, src);
-        const int sn = __shfl_sync(FULL, s, src);
-        const double ud = __shfl_up_sync(FULL, Ld, 1);
-        const int us = __shfl_up_sync(FULL, Ls, 1);
-        const int pos = __popc(__ballot_sync(FULL, Ld <= Dn));
-        if (pos < k) {
-            if (lane > pos) { Ld = ud; Ls = us; }
-            if (lane == pos) { Ld = Dn; Ls = sn; }
-            if (lane >= k) { Ld = CUDART_INF; Ls = 0x7fffffff; }
-            thr = min(thr, hi_word(__shfl_sync(FULL, Ld, k - 1)));
-        }
-    }
-}
-
 // Weights of C5: lane j < k holds d2_j. Returns w_j (0 for lanes >= k).
 // exact == true: fp64 exp and the oracle's sequential normalisation order;
 // exact == false (phase-2 tables, stored as fp32): fp32 exp and a tree sum.
@@ -175,126 +150,225 @@ __device__ __forceinline__ double simplex_weight(double d2, int k, int lane) {
     return __ddiv_rn(u, sum);
 }
 
+constexpr double PAD_VALUE = 1e300;   // (q - PAD)^2 = +inf: out-of-range coordinates poison D
+constexpr int THR_EMPTY = 0x7fefffff; // hi word of the largest finite double (rejects +inf)
+__host__ __device__ constexpr int knn_padl(int tau) { return (ECAP - 1) * tau; }
+constexpr int KNN_PADR = 32;
+// Per-warp shared-memory state: the sorted top-(E+1) list of every E (entry j of list e at
+// loff(e) + j, k = e + 2 entries), the per-E prefilter bounds and a [ECAP][32] scratch of the
+// candidate distances that passed the prefilter in the current chunk.
+__host__ __device__ constexpr int loff(int e) { return e * (e + 3) / 2; }
+constexpr int LIST_ENTRIES = loff(ECAP);  // 230
+struct KnnWarpSmem {
+    double D[LIST_ENTRIES];
+    int S[LIST_ENTRIES];
+    int thr[ECAP];
+    double scr[ECAP * 32];
+};
+constexpr size_t knn_smem_bytes(int L, int tau) {
+    return ((size_t)(knn_padl(tau) + L + KNN_PADR) * sizeof(double) + 15) / 16 * 16 +
+           (size_t)KNN_WARPS * ((sizeof(KnnWarpSmem) + 15) / 16 * 16);
+}
+
+// Insert the lanes flagged in `bal` (their distances are in W.scr[e][lane], their labels are
+// c0 + lane) into list e (k entries, sorted by (d2, s)). Candidates arrive in increasing s,
+// so an entry already in the list with an equal distance has a smaller index and stays in
+// front: the (d2, s) lexicographic order of C4 / S:137. A candidate whose position would be
+// >= k is rejected. After an accepted insertion the remaining flagged lanes are re-filtered
+// against the new k-th distance. Returns the new prefilter bound (hi word).
+__device__ __forceinline__ int list_insert(KnnWarpSmem& W, int e, unsigned bal, int c0, int lane, int thr) {
+    const int k = e + 2;
+    double* LD = W.D + loff(e);
+    int* LS = W.S + loff(e);
+    const double* scr = W.scr + e * 32;
+    while (bal) {
+        const int src = __ffs(bal) - 1;
+        bal &= bal - 1;
+        const double Dn = scr[src];
+        const double myD = lane < k ? LD[lane] : CUDART_INF;
+        const int myS = lane < k ? LS[lane] : 0x7fffffff;
+        const int pos = __popc(__ballot_sync(FULL, myD <= Dn));
+        if (pos < k) {
+            const double upD = __shfl_up_sync(FULL, myD, 1);
+            const int upS = __shfl_up_sync(FULL, myS, 1);
+            const double nD = lane > pos ? upD : (lane == pos ? Dn : myD);
+            const int nS = lane > pos ? upS : (lane == pos ? c0 + src : myS);
+            __syncwarp();
+            if (lane < k) { LD[lane] = nD; LS[lane] = nS; }
+            thr = min(thr, hi_word(__shfl_sync(FULL, nD, k - 1)));
+            bal &= __ballot_sync(FULL, hi_word(scr[lane]) <= thr);
+        }
+        __syncwarp();
+    }
+    return thr;
+}
+
 // One warp, queries t = t_begin .. t_end-1 in order. For each query: D_E(t, s) for E = 1..Eq
 // accumulated incrementally over E (D_E = D_{E-1} + (a[t-(E-1)tau] - b[s-(E-1)tau])^2, the
 // same fp64 operation sequence as the oracle's C3 loop, so every D_E is bit-identical to the
 // oracle's) and, at every E in the selected set, a top-(E+1) list by (D_E, s).
+// Candidates outside P_E are never tested explicitly: the candidate series is padded on
+// both sides with PAD_VALUE, so a coordinate before the series start makes D = +inf from
+// that E on, and lanes past the candidate range / the excluded self start at D = +inf.
+// The sweep is branch-free per E: each E only compares against its prefilter bound and
+// records passing lanes; list insertions for all E run afterwards in one shared code path.
 //
-// Seeded thresholds (E >= 3): the successors s+1 of query t-1's neighbours at the same E
-// are usually near neighbours of t (the dynamics carries neighbourhoods along). Their exact
-// distances D_E(t, s+1) give k distinct evaluated candidates, so their maximum is an upper
-// bound on the k-th smallest distance; candidates above it can never enter the list and
-// are filtered before the insertion path. This changes the work, not the result.
-template <int MODE>
-__device__ __forceinline__ void knn_warp(const KnnParams& P, const double* __restrict__ qa,
+// Seeded bounds (E >= 3): the successors s+1 of query t-1's neighbours at the same E are
+// usually near neighbours of t (the dynamics carries neighbourhoods along). Their exact
+// distances D_E(t, s+1) give k distinct evaluated candidates, so their maximum bounds the
+// k-th smallest distance; candidates above it can never enter the list and are filtered
+// before the insertion path. This changes the work, not the result.
+template <int MODE, bool TAU1, bool FULLMASK>
+__device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, const double* __restrict__ qa,
                                          const double* __restrict__ cb, int t_begin, int t_end, int ncand,
                                          unsigned mask, int Etop, int b, int lane) {
-    const int tau = P.tau;
+    const int tau = TAU1 ? 1 : P.tau;
     const bool excl = (MODE != MODE_SIMPLEX) && P.excl;
-    double Ld[ECAP];
-    int Ls[ECAP], thr[ECAP];
-#pragma unroll
-    for (int e = 0; e < ECAP; ++e) { Ld[e] = CUDART_INF; Ls[e] = 0x7fffffff; }
+    auto selected = [&](int e) { return FULLMASK || ((mask >> (e + 1)) & 1u); };
     int prevEq = 0;  // lists hold the final neighbours of query t-1 for E <= prevEq
     for (int t = t_begin; t < t_end; ++t) {
         const int Eq = min(Etop, t / tau + 1);  // E with (E-1) tau <= t
-        double q[ECAP];
-#pragma unroll
-        for (int e = 0; e < ECAP; ++e) q[e] = (e < Eq) ? qa[t - e * tau] : 0.0;
-        // ---- seeded thresholds from the previous query's lists, then reset the lists
-#pragma unroll
-        for (int e = 0; e < ECAP; ++e) {
-            thr[e] = 0x7ff00000;  // hi word of +inf
-            if (e >= 2 && e < Eq && e < prevEq && ((mask >> (e + 1)) & 1u)) {
+        // ---- seeded bounds from the previous query's lists, then reset the lists
+        for (int e = 0; e < Eq; ++e) {
+            int th = THR_EMPTY;
+            if (e >= 2 && e < prevEq && selected(e)) {
                 const int k = e + 2;
-                const int c = Ls[e] + 1;
+                const int c = (lane < k ? W.S[loff(e) + lane] : 0) + 1;
                 const bool ok = lane < k && c < ncand && c - e * tau >= 0 && !(excl && c == t);
-                double D = CUDART_INF;
-                if (ok) {
-                    D = 0.0;
-#pragma unroll
+                double D = 0.0;
+                if (ok)
                     for (int m = 0; m <= e; ++m) {
-                        const double diff = __dsub_rn(q[m], cb[c - m * tau]);
+                        const double diff = __dsub_rn(qa[t - m * tau], cb[c - m * tau]);
                         D = __dadd_rn(D, __dmul_rn(diff, diff));
                     }
-                }
-                const unsigned okb = __ballot_sync(FULL, ok);
-                if (okb == ((1u << k) - 1u)) {
-                    double th = lane < k ? D : 0.0;
+                if (__ballot_sync(FULL, ok) == ((1u << k) - 1u)) {
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) th = fmax(th, __shfl_xor_sync(FULL, th, o));
-                    thr[e] = hi_word(th);
+                    for (int o = 16; o > 0; o >>= 1) D = fmax(D, __shfl_xor_sync(FULL, D, o));
+                    th = hi_word(D);
                 }
             }
-            Ld[e] = CUDART_INF;
-            Ls[e] = 0x7fffffff;
+            __syncwarp();
+            if (lane == 0) W.thr[e] = th;
+            if (lane < e + 2) { W.D[loff(e) + lane] = CUDART_INF; W.S[loff(e) + lane] = 0x7fffffff; }
+        }
+        __syncwarp();
+        double q[ECAP];
+        int thr[ECAP];
+#pragma unroll
+        for (int e = 0; e < ECAP; ++e) {
+            q[e] = (e < Eq) ? qa[t - e * tau] : 0.0;
+            thr[e] = (e < Eq) ? W.thr[e] : 0;
         }
         // ---- sweep over the candidates in increasing s
-        for (int c0 = 0; c0 < ncand; c0 += 32) {
-            const int s = c0 + lane;
-            const bool valid = (s < ncand) && !(excl && s == t);
-            double D = 0.0;
+        auto flush = [&](int c0, unsigned pass) {
+            // list insertions for every E that had a passing lane in this chunk
+            unsigned om = __reduce_or_sync(FULL, pass);
+            __syncwarp();
+            while (om) {
+                const int e = __ffs(om) - 1;
+                om &= om - 1;
+                const unsigned bal = __ballot_sync(FULL, (pass >> e) & 1u);
+                const int nt = list_insert(W, e, bal, c0, lane, W.thr[e]);
+                if (lane == 0) W.thr[e] = nt;
+            }
+            __syncwarp();
 #pragma unroll
-            for (int e = 0; e < ECAP; ++e) {
-                if (e < Eq) {
-                    const int sm = s - e * tau;
-                    const bool ve = valid && sm >= 0;
-                    const double xv = cb[max(min(sm, ncand - 1), 0)];
-                    const double diff = __dsub_rn(q[e], xv);
+            for (int e = 0; e < ECAP; ++e)
+                if (e < Eq) thr[e] = W.thr[e];
+        };
+        if (FULLMASK && Eq == ECAP) {
+            // main path: every E = 1..ECAP kept, fully unrolled without per-E tests
+            for (int c0 = 0; c0 < ncand; c0 += 32) {
+                const int s = c0 + lane;
+                const double* cs = cb + s;  // padded: cs[-e*tau] is addressable for e < ECAP
+                double D = (s < ncand && !(excl && s == t)) ? 0.0 : CUDART_INF;
+                unsigned pass = 0u;
+#pragma unroll
+                for (int e = 0; e < ECAP; ++e) {
+                    const double diff = __dsub_rn(q[e], cs[-e * tau]);
                     D = __dadd_rn(D, __dmul_rn(diff, diff));
-                    if ((mask >> (e + 1)) & 1u) {
-                        // prefilter on the high word: D <= theta implies hi(D) <= hi(theta) (D >= 0)
-                        const unsigned bal = __ballot_sync(FULL, ve && hi_word(D) <= thr[e]);
-                        if (bal) list_insert(bal, D, s, e + 2, lane, Ld[e], Ls[e], thr[e]);
+                    // prefilter on the high word: D <= theta implies hi(D) <= hi(theta) (D >= 0)
+                    if (hi_word(D) <= thr[e]) {
+                        W.scr[e * 32 + lane] = D;
+                        pass |= 1u << e;
                     }
                 }
+                if (__any_sync(FULL, pass != 0u)) flush(c0, pass);
+            }
+        } else {
+            for (int c0 = 0; c0 < ncand; c0 += 32) {
+                const int s = c0 + lane;
+                const double* cs = cb + s;
+                double D = (s < ncand && !(excl && s == t)) ? 0.0 : CUDART_INF;
+                unsigned pass = 0u;
+#pragma unroll
+                for (int e = 0; e < ECAP; ++e) {
+                    if (e < Eq) {
+                        const double diff = __dsub_rn(q[e], cs[-e * tau]);
+                        D = __dadd_rn(D, __dmul_rn(diff, diff));
+                        if (selected(e) && hi_word(D) <= thr[e]) {
+                            W.scr[e * 32 + lane] = D;
+                            pass |= 1u << e;
+                        }
+                    }
+                }
+                if (__any_sync(FULL, pass != 0u)) flush(c0, pass);
             }
         }
         // ---- finalise every selected E of this query
-#pragma unroll
-        for (int e = 0; e < ECAP; ++e) {
-            if (e < Eq && ((mask >> (e + 1)) & 1u)) {
-                const int k = e + 2;
-                const int row = t - e * tau;
-                if (MODE == MODE_CCM) {
-                    const double w = simplex_weight<false>(Ld[e], k, lane);
-                    const int kp = kpad(k);
-                    if (lane < kp) {
-                        uint2 ent = lane < k ? make_uint2((unsigned)(Ls[e] + P.Tp), __float_as_uint((float)w))
-                                             : make_uint2(0u, 0u);
-                        P.tables[(int64_t)b * P.T_lib + P.offE[e + 1] + (int64_t)row * kp + lane] = ent;
-                    }
-                } else if (MODE == MODE_EMBED) {
-                    const double w = simplex_weight<true>(Ld[e], k, lane);
-                    if (lane < k) {
-                        P.out_idx[(int64_t)row * k + lane] = Ls[e];
-                        P.out_dist[(int64_t)row * k + lane] = (float)sqrt(Ld[e]);
-                        if (P.out_w) P.out_w[(int64_t)row * k + lane] = (float)w;
-                    }
-                } else {  // MODE_SIMPLEX: forecast one step ahead, yhat = sum_k w_k lib[s_k + 1]
-                    const double w = simplex_weight<true>(Ld[e], k, lane);
-                    const double prod = lane < k ? __dmul_rn(w, cb[Ls[e] + 1]) : 0.0;
-                    double acc = 0.0;
-                    for (int j = 0; j < k; ++j) acc = __dadd_rn(acc, __shfl_sync(FULL, prod, j));
-                    if (lane == 0) P.pred[((int64_t)b * ECAP + e) * P.LQ + t] = acc;
+        for (int e = 0; e < Eq; ++e) {
+            if (!selected(e)) continue;
+            const int k = e + 2;
+            const int row = t - e * tau;
+            const double d2 = lane < k ? W.D[loff(e) + lane] : CUDART_INF;
+            const int sl = lane < k ? W.S[loff(e) + lane] : 0;
+            if (MODE == MODE_CCM) {
+                const double w = simplex_weight<false>(d2, k, lane);
+                const int kp = kpad(k);
+                if (lane < kp) {
+                    uint2 ent = lane < k ? make_uint2((unsigned)(sl + P.Tp), __float_as_uint((float)w))
+                                         : make_uint2(0u, 0u);
+                    P.tables[(int64_t)b * P.T_lib + P.offE[e + 1] + (int64_t)row * kp + lane] = ent;
                 }
+            } else if (MODE == MODE_EMBED) {
+                const double w = simplex_weight<true>(d2, k, lane);
+                if (lane < k) {
+                    P.out_idx[(int64_t)row * k + lane] = sl;
+                    P.out_dist[(int64_t)row * k + lane] = (float)sqrt(d2);
+                    if (P.out_w) P.out_w[(int64_t)row * k + lane] = (float)w;
+                }
+            } else {  // MODE_SIMPLEX: forecast one step ahead, yhat = sum_k w_k lib[s_k + 1]
+                const double w = simplex_weight<true>(d2, k, lane);
+                const double prod = lane < k ? __dmul_rn(w, cb[sl + 1]) : 0.0;
+                double acc = 0.0;
+                for (int j = 0; j < k; ++j) acc = __dadd_rn(acc, __shfl_sync(FULL, prod, j));
+                if (lane == 0) P.pred[((int64_t)b * ECAP + e) * P.LQ + t] = acc;
             }
         }
         prevEq = Eq;
     }
 }
 
-// grid = (ceil(nq / KNN_QPB), slots); block = KNN_WARPS * 32; dynamic smem = L doubles.
+// grid = (ceil(nq / KNN_QPB), slots); block = KNN_WARPS * 32; dynamic smem = knn_smem_bytes.
 // Warp w of CTA x handles the contiguous queries [x*QPB + w*QPW, +QPW) (so that each query
-// can seed its thresholds from the previous one).
-template <int MODE>
+// can seed its bounds from the previous one).
+template <int MODE, bool TAU1, bool FULLMASK>
 __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnParams P) {
-    extern __shared__ double xs[];
+    extern __shared__ __align__(16) unsigned char knn_smem[];
+    double* xs_pad = reinterpret_cast<double*>(knn_smem);
     const int b = blockIdx.y;
     const int row = P.slot_series ? P.slot_series[b] : b;
     const float* xg = P.X + (int64_t)row * P.ldx;
-    for (int i = threadIdx.x; i < P.L; i += blockDim.x) xs[i] = (double)xg[i];
+    const int padl = knn_padl(P.tau);
+    const int nx = padl + P.L + KNN_PADR;
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+        const int t = i - padl;
+        xs_pad[i] = (t >= 0 && t < P.L) ? (double)xg[t] : PAD_VALUE;
+    }
     __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    KnnWarpSmem& W = reinterpret_cast<KnnWarpSmem*>(knn_smem + ((size_t)nx * sizeof(double) + 15) / 16 * 16)[warp];
+    const double* xs = xs_pad + padl;
     unsigned mask = P.maskS;
     int Etop = P.Etop;
     if (P.slotE) {
@@ -315,10 +389,9 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnPa
         qa = cb = xs;
         nq = ncand = P.L - P.Tp;          // P_1 = [0, L-1-Tp]; per-E lower bound (E-1)tau
     }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int t0 = blockIdx.x * KNN_QPB + warp * KNN_QPW;
     const int t1 = min(nq, t0 + KNN_QPW);
-    if (t0 < t1) knn_warp<MODE>(P, qa, cb, t0, t1, ncand, mask, Etop, b, lane);
+    if (t0 < t1) knn_warp<MODE, TAU1, FULLMASK>(P, W, qa, cb, t0, t1, ncand, mask, Etop, b, lane);
 }
 
 // ------------------------------------------------------------------ S2 / S3 phase-1 skill

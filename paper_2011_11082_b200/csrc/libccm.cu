@@ -166,15 +166,25 @@ CcmWs ccm_ws(void* base, int N, int L, int tau, int Tp) {
     return w;
 }
 
-template <int MODE>
-edm_status launch_knn(const KnnParams& P, int nq, int slots, size_t smem, cudaStream_t st) {
-    static_assert(MODE >= 0, "");
-    if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(knn_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    dim3 grid((nq + KNN_QPB - 1) / KNN_QPB, slots);
+template <int MODE, bool TAU1, bool FULL>
+edm_status launch_knn_t(const KnnParams& P, dim3 grid, size_t smem, cudaStream_t st) {
+    if (smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(knn_kernel<MODE, TAU1, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     PROF_LAUNCH(MODE == MODE_CCM ? EDM_PROF_CCM_KNN : MODE == MODE_SIMPLEX ? EDM_PROF_SIMPLEX_KNN : EDM_PROF_OTHER, st,
-                knn_kernel<MODE><<<grid, KNN_WARPS * 32, smem, st>>>(P));
+                knn_kernel<MODE, TAU1, FULL><<<grid, KNN_WARPS * 32, smem, st>>>(P));
     LAUNCH_CHECK("knn_kernel");
     return EDM_OK;
+}
+
+// Picks the specialisation: tau == 1 (constant-offset shared loads) and whether every E in
+// 1..Etop is selected (no per-E membership test).
+template <int MODE>
+edm_status launch_knn(const KnnParams& P, int nq, int slots, cudaStream_t st) {
+    dim3 grid((nq + KNN_QPB - 1) / KNN_QPB, slots);
+    const size_t smem = knn_smem_bytes(P.L, P.tau);
+    const bool full = !P.slotE && P.Etop >= 1 && P.maskS == ((2u << P.Etop) - 2u);
+    if (P.tau == 1) return full ? launch_knn_t<MODE, true, true>(P, grid, smem, st) : launch_knn_t<MODE, true, false>(P, grid, smem, st);
+    return full ? launch_knn_t<MODE, false, true>(P, grid, smem, st) : launch_knn_t<MODE, false, false>(P, grid, smem, st);
 }
 
 }  // namespace
@@ -236,7 +246,7 @@ edm_status edm_embed_knn(const float* series, int32_t L, int32_t E, int32_t tau,
     P.maskS = 1u << E;
     P.Etop = E;
     P.out_idx = idx; P.out_dist = dist; P.out_w = w;
-    return launch_knn<MODE_EMBED>(P, L - Tp, 1, (size_t)L * sizeof(double), (cudaStream_t)stream);
+    return launch_knn<MODE_EMBED>(P, L - Tp, 1, (cudaStream_t)stream);
 }
 
 edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int32_t s_begin, int32_t s_end,
@@ -271,7 +281,7 @@ edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int
             KnnParams P{};
             P.X = W.Xs; P.ldx = L; P.L = L; P.tau = tau; P.Tp = 1; P.excl = 0;
             P.maskS = mask; P.Etop = Etop; P.pred = W.pred; P.LQ = LQ;
-            st = launch_knn<MODE_SIMPLEX>(P, std::max(Ltgt - 1, 1), nb, (size_t)L * sizeof(double), cs);
+            st = launch_knn<MODE_SIMPLEX>(P, std::max(Ltgt - 1, 1), nb, cs);
             if (st != EDM_OK) return st;
         }
         const int nthr = nb * E_max;
@@ -382,7 +392,7 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int3
         P.slotE = (mode == EDM_E_LIBRARY) ? W.slotE + r0 : nullptr;
         P.tables = W.tables; P.T_lib = T_lib;
         memcpy(P.offE, offE, sizeof(offE));
-        st = launch_knn<MODE_CCM>(P, L - Tp, nb, (size_t)L * sizeof(double), cs);
+        st = launch_knn<MODE_CCM>(P, L - Tp, nb, cs);
         if (st != EDM_OK) return st;
         LookupParams Q{};
         Q.Yp = W.Yp; Q.Np = Np; Q.colmap = W.colmap;
