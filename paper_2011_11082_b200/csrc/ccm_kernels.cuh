@@ -175,31 +175,31 @@ constexpr size_t knn_smem_bytes(int L, int tau) {
 // so an entry already in the list with an equal distance has a smaller index and stays in
 // front: the (d2, s) lexicographic order of C4 / S:137. A candidate whose position would be
 // >= k is rejected. After an accepted insertion the remaining flagged lanes are re-filtered
-// against the new k-th distance. Returns the new prefilter bound (hi word).
+// against the new k-th distance. The list lives in registers (lane j = entry j) for the
+// duration of the call. Returns the new prefilter bound (hi word).
 __device__ __forceinline__ int list_insert(KnnWarpSmem& W, int e, unsigned bal, int c0, int lane, int thr) {
     const int k = e + 2;
     double* LD = W.D + loff(e);
     int* LS = W.S + loff(e);
     const double* scr = W.scr + e * 32;
-    while (bal) {
+    double myD = lane < k ? LD[lane] : CUDART_INF;
+    int myS = lane < k ? LS[lane] : 0x7fffffff;
+    const int candHi = hi_word(scr[lane]);
+    do {
         const int src = __ffs(bal) - 1;
         bal &= bal - 1;
         const double Dn = scr[src];
-        const double myD = lane < k ? LD[lane] : CUDART_INF;
-        const int myS = lane < k ? LS[lane] : 0x7fffffff;
         const int pos = __popc(__ballot_sync(FULL, myD <= Dn));
         if (pos < k) {
             const double upD = __shfl_up_sync(FULL, myD, 1);
             const int upS = __shfl_up_sync(FULL, myS, 1);
-            const double nD = lane > pos ? upD : (lane == pos ? Dn : myD);
-            const int nS = lane > pos ? upS : (lane == pos ? c0 + src : myS);
-            __syncwarp();
-            if (lane < k) { LD[lane] = nD; LS[lane] = nS; }
-            thr = min(thr, hi_word(__shfl_sync(FULL, nD, k - 1)));
-            bal &= __ballot_sync(FULL, hi_word(scr[lane]) <= thr);
+            if (lane == pos) { myD = Dn; myS = c0 + src; }
+            else if (lane > pos) { myD = upD; myS = upS; }
+            thr = min(thr, __shfl_sync(FULL, hi_word(myD), k - 1));
+            bal &= __ballot_sync(FULL, candHi <= thr);
         }
-        __syncwarp();
-    }
+    } while (bal);
+    if (lane < k) { LD[lane] = myD; LS[lane] = myS; }
     return thr;
 }
 
@@ -264,13 +264,13 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, con
             // list insertions for every E that had a passing lane in this chunk
             unsigned om = __reduce_or_sync(FULL, pass);
             __syncwarp();
-            while (om) {
+            do {
                 const int e = __ffs(om) - 1;
                 om &= om - 1;
                 const unsigned bal = __ballot_sync(FULL, (pass >> e) & 1u);
                 const int nt = list_insert(W, e, bal, c0, lane, W.thr[e]);
                 if (lane == 0) W.thr[e] = nt;
-            }
+            } while (om);
             __syncwarp();
 #pragma unroll
             for (int e = 0; e < ECAP; ++e)

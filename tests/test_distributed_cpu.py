@@ -1,0 +1,74 @@
+"""The multi-GPU host logic (sharding, all-gather of E, gather of rho rows) on CPU with the
+gloo backend at world_size 2 and 3. The per-rank phase functions are the fp64 oracle
+here (the CUDA kernels need a GPU); the test checks that the sharded map equals the
+single-process oracle map exactly (byte-identical at any world size)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2011_11082_b200 import distributed as D
+from paper_2011_11082_b200 import synth
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_fns():
+    from oracle import oracle as O
+
+    def simplex_fn(data, E_max, tau, s0, s1):
+        e, _ = O.simplex_all(data.numpy(), E_max, tau, s0, s1, nthreads=1)
+        return torch.from_numpy(e)
+
+    def ccm_fn(data, E, tau, Tp, mode, excl, l0, l1):
+        r = O.ccm_rows(data.numpy(), E.numpy(), tau, Tp, 0 if mode == "target" else 1, excl, l0, l1, nthreads=1)
+        return torch.from_numpy(r.astype(np.float32))
+
+    return simplex_fn, ccm_fn
+
+
+def _worker(rank, world, port, data, out_path, mode):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sf, cf = _oracle_fns()
+    E, rows, full = D.run(torch.from_numpy(data), 6, 1, 1, mode, True, sf, cf, gather=True)
+    if rank == 0:
+        np.save(out_path + "_E.npy", E.numpy())
+        np.save(out_path + "_rho.npy", full.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_covers_everything():
+    for n in (1, 7, 64, 1001):
+        for w in (1, 2, 3, 8):
+            parts = [D.shard(n, r, w) for r in range(w)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(w - 1))
+            sizes = [b - a for a, b in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.parametrize("world,mode", [(2, "target"), (3, "library")])
+def test_sharded_map_equals_single_process(tmp_path, world, mode):
+    from oracle import oracle as O
+    data = synth.random_dataset(13, 70, 21)
+    out = str(tmp_path / "res")
+    mp.spawn(_worker, args=(world, _free_port(), data, out, mode), nprocs=world, join=True)
+    E = np.load(out + "_E.npy")
+    rho = np.load(out + "_rho.npy")
+    rE, _ = O.simplex_all(data, 6, 1)
+    assert np.array_equal(E, rE)
+    ref = O.ccm_rows(data, rE, 1, 1, 0 if mode == "target" else 1, True).astype(np.float32)
+    assert np.array_equal(rho.view(np.uint32), ref.view(np.uint32))
