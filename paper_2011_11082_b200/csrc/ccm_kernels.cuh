@@ -170,37 +170,44 @@ constexpr size_t knn_smem_bytes(int L, int tau) {
            (size_t)KNN_WARPS * ((sizeof(KnnWarpSmem) + 15) / 16 * 16);
 }
 
-// Insert the lanes flagged in `bal` (their distances are in W.scr[e][lane], their labels are
-// c0 + lane) into list e (k entries, sorted by (d2, s)). Candidates arrive in increasing s,
-// so an entry already in the list with an equal distance has a smaller index and stays in
-// front: the (d2, s) lexicographic order of C4 / S:137. A candidate whose position would be
-// >= k is rejected. After an accepted insertion the remaining flagged lanes are re-filtered
-// against the new k-th distance. The list lives in registers (lane j = entry j) for the
-// duration of the call. Returns the new prefilter bound (hi word).
-__device__ __forceinline__ int list_insert(KnnWarpSmem& W, int e, unsigned bal, int c0, int lane, int thr) {
+// Merge the lanes flagged in `bal` (this chunk's candidates that passed list e's prefilter;
+// distance in W.scr[e][lane], label c0 + lane) into list e (k entries sorted by the (d2, s)
+// lexicographic order of C4 / S:137). Candidates already in the list (prefilled from the
+// previous query, see knn_warp) are dropped first. Each list entry and each candidate then
+// computes its rank in the merged sequence (one broadcast per candidate) and the ones with
+// rank < k are written to their slot. Returns the hi word of the new k-th distance (+inf's
+// while the list is not full).
+__device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, int c0, int lane) {
     const int k = e + 2;
     double* LD = W.D + loff(e);
     int* LS = W.S + loff(e);
     const double* scr = W.scr + e * 32;
-    double myD = lane < k ? LD[lane] : CUDART_INF;
-    int myS = lane < k ? LS[lane] : 0x7fffffff;
-    const int candHi = hi_word(scr[lane]);
+    const bool isList = lane < k;
+    const double myD = isList ? LD[lane] : CUDART_INF;
+    const int myS = isList ? LS[lane] : 0x7fffffff;
+    const unsigned dl = (unsigned)(myS - c0);
+    bal &= ~__reduce_or_sync(FULL, (isList && dl < 32u) ? (1u << dl) : 0u);  // drop duplicates
+    if (!bal) return hi_word(LD[k - 1]);
+    const bool isCand = (bal >> lane) & 1u;
+    const double cand = scr[lane];
+    int nl = lane;  // rank of my list entry
+    int nc = 0;     // rank of my candidate
+    unsigned b = bal;
     do {
-        const int src = __ffs(bal) - 1;
-        bal &= bal - 1;
-        const double Dn = scr[src];
-        const int pos = __popc(__ballot_sync(FULL, myD <= Dn));
-        if (pos < k) {
-            const double upD = __shfl_up_sync(FULL, myD, 1);
-            const int upS = __shfl_up_sync(FULL, myS, 1);
-            if (lane == pos) { myD = Dn; myS = c0 + src; }
-            else if (lane > pos) { myD = upD; myS = upS; }
-            thr = min(thr, __shfl_sync(FULL, hi_word(myD), k - 1));
-            bal &= __ballot_sync(FULL, candHi <= thr);
-        }
-    } while (bal);
-    if (lane < k) { LD[lane] = myD; LS[lane] = myS; }
-    return thr;
+        const int j = __ffs(b) - 1;
+        b &= b - 1;
+        const double Dj = scr[j];
+        const int sj = c0 + j;
+        const int pl = __popc(__ballot_sync(FULL, myD < Dj || (myD == Dj && myS < sj)));
+        if (lane == j) nc += pl;
+        nl += (Dj < myD || (Dj == myD && sj < myS)) ? 1 : 0;
+        nc += (Dj < cand || (Dj == cand && j < lane)) ? 1 : 0;
+    } while (b);
+    __syncwarp();
+    if (isList && nl < k) { LD[nl] = myD; LS[nl] = myS; }
+    if (isCand && nc < k) { LD[nc] = cand; LS[nc] = c0 + lane; }
+    __syncwarp();
+    return hi_word(LD[k - 1]);
 }
 
 // One warp, queries t = t_begin .. t_end-1 in order. For each query: D_E(t, s) for E = 1..Eq
@@ -213,11 +220,12 @@ __device__ __forceinline__ int list_insert(KnnWarpSmem& W, int e, unsigned bal, 
 // The sweep is branch-free per E: each E only compares against its prefilter bound and
 // records passing lanes; list insertions for all E run afterwards in one shared code path.
 //
-// Seeded bounds (E >= 3): the successors s+1 of query t-1's neighbours at the same E are
-// usually near neighbours of t (the dynamics carries neighbourhoods along). Their exact
-// distances D_E(t, s+1) give k distinct evaluated candidates, so their maximum bounds the
-// k-th smallest distance; candidates above it can never enter the list and are filtered
-// before the insertion path. This changes the work, not the result.
+// Prefilled lists: the successors s+1 of query t-1's k neighbours at the same E are usually
+// near neighbours of t (the dynamics carries neighbourhoods along). They are distinct valid
+// candidates, so the list starts as their exact (d2, s)-sorted set and its k-th distance
+// bounds the final one; the sweep filters against that bound and merges the few candidates
+// that beat it (duplicates of prefilled entries are dropped). This changes the work, not the
+// result: the final list is the k smallest keys over all candidates either way.
 template <int MODE, bool TAU1, bool FULLMASK>
 __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, const double* __restrict__ qa,
                                          const double* __restrict__ cb, int t_begin, int t_end, int ncand,
@@ -228,28 +236,41 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, con
     int prevEq = 0;  // lists hold the final neighbours of query t-1 for E <= prevEq
     for (int t = t_begin; t < t_end; ++t) {
         const int Eq = min(Etop, t / tau + 1);  // E with (E-1) tau <= t
-        // ---- seeded bounds from the previous query's lists, then reset the lists
+        // ---- prefill every list from the previous query: the successors s+1 of query t-1's
+        // k neighbours at the same E, with their exact distances D_E(t, s+1), sorted by
+        // (d2, s) (rank counting). The sweep then only has to merge candidates that beat them.
         for (int e = 0; e < Eq; ++e) {
-            int th = THR_EMPTY;
-            if (e >= 2 && e < prevEq && selected(e)) {
-                const int k = e + 2;
-                const int c = (lane < k ? W.S[loff(e) + lane] : 0) + 1;
-                const bool ok = lane < k && c < ncand && c - e * tau >= 0 && !(excl && c == t);
-                double D = 0.0;
-                if (ok)
-                    for (int m = 0; m <= e; ++m) {
-                        const double diff = __dsub_rn(qa[t - m * tau], cb[c - m * tau]);
-                        D = __dadd_rn(D, __dmul_rn(diff, diff));
-                    }
-                if (__ballot_sync(FULL, ok) == ((1u << k) - 1u)) {
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) D = fmax(D, __shfl_xor_sync(FULL, D, o));
-                    th = hi_word(D);
+            if (!selected(e)) continue;
+            const int k = e + 2;
+            double* LD = W.D + loff(e);
+            int* LS = W.S + loff(e);
+            const int c = (lane < k ? LS[lane] : 0) + 1;
+            const bool ok = lane < k && e < prevEq && c < ncand && c - e * tau >= 0 && !(excl && c == t);
+            const bool all = __ballot_sync(FULL, ok) == ((1u << k) - 1u);
+            double D = CUDART_INF;
+            if (all && ok) {
+                D = 0.0;
+                for (int m = 0; m <= e; ++m) {
+                    const double diff = __dsub_rn(qa[t - m * tau], cb[c - m * tau]);
+                    D = __dadd_rn(D, __dmul_rn(diff, diff));
+                }
+            }
+            int rank = lane;
+            if (all) {
+                rank = 0;
+                for (int i = 0; i < k; ++i) {
+                    const double Di = __shfl_sync(FULL, D, i);
+                    const int ci = __shfl_sync(FULL, c, i);
+                    rank += (Di < D || (Di == D && ci < c)) ? 1 : 0;
                 }
             }
             __syncwarp();
-            if (lane == 0) W.thr[e] = th;
-            if (lane < e + 2) { W.D[loff(e) + lane] = CUDART_INF; W.S[loff(e) + lane] = 0x7fffffff; }
+            if (lane < k) {
+                LD[rank] = all ? D : CUDART_INF;
+                LS[rank] = all ? c : 0x7fffffff;
+            }
+            __syncwarp();
+            if (lane == 0) W.thr[e] = all ? min(THR_EMPTY, hi_word(LD[k - 1])) : THR_EMPTY;
         }
         __syncwarp();
         double q[ECAP];
@@ -268,7 +289,7 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, con
                 const int e = __ffs(om) - 1;
                 om &= om - 1;
                 const unsigned bal = __ballot_sync(FULL, (pass >> e) & 1u);
-                const int nt = list_insert(W, e, bal, c0, lane, W.thr[e]);
+                const int nt = min(W.thr[e], list_merge(W, e, bal, c0, lane));
                 if (lane == 0) W.thr[e] = nt;
             } while (om);
             __syncwarp();
