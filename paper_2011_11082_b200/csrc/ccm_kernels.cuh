@@ -155,48 +155,56 @@ constexpr int THR_EMPTY = 0x7fefffff; // hi word of the largest finite double (r
 __host__ __device__ constexpr int knn_padl(int tau) { return (ECAP - 1) * tau; }
 constexpr int KNN_PADR = 32;
 // Per-warp shared-memory state: the sorted top-(E+1) list of every E (entry j of list e at
-// loff(e) + j, k = e + 2 entries), the per-E prefilter bounds and a [ECAP][32] scratch of the
-// candidate distances that passed the prefilter in the current chunk.
+// loff(e) + j, k = e + 2 entries) and the per-E prefilter bounds.
 __host__ __device__ constexpr int loff(int e) { return e * (e + 3) / 2; }
 constexpr int LIST_ENTRIES = loff(ECAP);  // 230
 struct KnnWarpSmem {
     double D[LIST_ENTRIES];
     int S[LIST_ENTRIES];
     int thr[ECAP];
-    double scr[ECAP * 32];
 };
+// Per-warp membership words memb[s] (bit e <=> candidate s was prefilled into list e): the
+// sweep drops those (candidate, E) pairs, which are already in the list with their exact
+// distance. Allocated for L <= KNN_MEMB_MAXL; longer series fall back to the duplicate check
+// inside list_merge.
+constexpr int KNN_MEMB_MAXL = 2048;
+__host__ __device__ constexpr int knn_memb_words(int L) { return L <= KNN_MEMB_MAXL ? (L + 64 + 3) / 4 * 4 : 0; }
+__host__ __device__ constexpr size_t knn_warp_bytes(int L) {
+    return (sizeof(KnnWarpSmem) + 15) / 16 * 16 + (size_t)knn_memb_words(L) * sizeof(unsigned);
+}
 constexpr size_t knn_smem_bytes(int L, int tau) {
     return ((size_t)(knn_padl(tau) + L + KNN_PADR) * sizeof(double) + 15) / 16 * 16 +
-           (size_t)KNN_WARPS * ((sizeof(KnnWarpSmem) + 15) / 16 * 16);
+           (size_t)KNN_WARPS * knn_warp_bytes(L);
 }
 
 // Merge the lanes flagged in `bal` (this chunk's candidates that passed list e's prefilter;
-// distance in W.scr[e][lane], label c0 + lane) into list e (k entries sorted by the (d2, s)
-// lexicographic order of C4 / S:137). Candidates already in the list (prefilled from the
-// previous query, see knn_warp) are dropped first. Each list entry and each candidate then
-// computes its rank in the merged sequence (one broadcast per candidate) and the ones with
-// rank < k are written to their slot. Returns the hi word of the new k-th distance (+inf's
-// while the list is not full).
-__device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, int c0, int lane) {
+// distance `cand` in the lane's register, label c0 + lane) into list e (k entries sorted by
+// the (d2, s) lexicographic order of C4 / S:137). Candidates already in the list (prefilled
+// from the previous query, see knn_warp) are dropped first when no membership words exist.
+// Each list entry and each candidate then computes its rank in the merged sequence (one
+// broadcast per candidate) and the ones with rank < k are written to their slot. Returns the
+// hi word of the new k-th distance (+inf's while the list is not full).
+__device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, double cand, int c0, int lane,
+                                          bool dedup) {
     const int k = e + 2;
     double* LD = W.D + loff(e);
     int* LS = W.S + loff(e);
-    const double* scr = W.scr + e * 32;
     const bool isList = lane < k;
     const double myD = isList ? LD[lane] : CUDART_INF;
     const int myS = isList ? LS[lane] : 0x7fffffff;
-    const unsigned dl = (unsigned)(myS - c0);
-    bal &= ~__reduce_or_sync(FULL, (isList && dl < 32u) ? (1u << dl) : 0u);  // drop duplicates
-    if (!bal) return hi_word(LD[k - 1]);
+    if (dedup) {
+        const unsigned dl = (unsigned)(myS - c0);
+        bal &= ~__reduce_or_sync(FULL, (isList && dl < 32u) ? (1u << dl) : 0u);
+        if (!bal) return hi_word(LD[k - 1]);
+    }
     const bool isCand = (bal >> lane) & 1u;
-    const double cand = scr[lane];
     int nl = lane;  // rank of my list entry
     int nc = 0;     // rank of my candidate
     unsigned b = bal;
     do {
         const int j = __ffs(b) - 1;
         b &= b - 1;
-        const double Dj = scr[j];
+        const double Dj = __shfl_sync(FULL, cand, j);
         const int sj = c0 + j;
         const int pl = __popc(__ballot_sync(FULL, myD < Dj || (myD == Dj && myS < sj)));
         if (lane == j) nc += pl;
@@ -227,7 +235,8 @@ __device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, i
 // that beat it (duplicates of prefilled entries are dropped). This changes the work, not the
 // result: the final list is the k smallest keys over all candidates either way.
 template <int MODE, bool TAU1, bool FULLMASK>
-__device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, const double* __restrict__ qa,
+__device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, unsigned* memb, int mw,
+                                         const double* __restrict__ qa,
                                          const double* __restrict__ cb, int t_begin, int t_end, int ncand,
                                          unsigned mask, int Etop, int b, int lane) {
     const int tau = TAU1 ? 1 : P.tau;
@@ -239,6 +248,11 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, con
         // ---- prefill every list from the previous query: the successors s+1 of query t-1's
         // k neighbours at the same E, with their exact distances D_E(t, s+1), sorted by
         // (d2, s) (rank counting). The sweep then only has to merge candidates that beat them.
+        if (memb) {
+            for (int i = lane * 4; i < mw; i += 128)
+                *reinterpret_cast<uint4*>(memb + i) = make_uint4(0u, 0u, 0u, 0u);
+            __syncwarp();
+        }
         for (int e = 0; e < Eq; ++e) {
             if (!selected(e)) continue;
             const int k = e + 2;
@@ -268,6 +282,7 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, con
             if (lane < k) {
                 LD[rank] = all ? D : CUDART_INF;
                 LS[rank] = all ? c : 0x7fffffff;
+                if (all && memb) atomicOr(memb + c, 1u << e);
             }
             __syncwarp();
             if (lane == 0) W.thr[e] = all ? min(THR_EMPTY, hi_word(LD[k - 1])) : THR_EMPTY;
@@ -282,16 +297,23 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, con
         }
         // ---- sweep over the candidates in increasing s
         auto flush = [&](int c0, unsigned pass) {
-            // list insertions for every E that had a passing lane in this chunk
+            // list merges for every E that had a passing lane in this chunk; the candidate
+            // distances are recomputed (same operation sequence) up to the largest such E
             unsigned om = __reduce_or_sync(FULL, pass);
-            __syncwarp();
-            do {
-                const int e = __ffs(om) - 1;
-                om &= om - 1;
-                const unsigned bal = __ballot_sync(FULL, (pass >> e) & 1u);
-                const int nt = min(W.thr[e], list_merge(W, e, bal, c0, lane));
-                if (lane == 0) W.thr[e] = nt;
-            } while (om);
+            const int s = c0 + lane;
+            const double* cs = cb + s;
+            const double* qt = qa + t;
+            double D = (s < ncand && !(excl && s == t)) ? 0.0 : CUDART_INF;
+            const int elast = 31 - __clz(om);
+            for (int e = 0; e <= elast; ++e) {
+                const double diff = __dsub_rn(qt[-e * tau], cs[-e * tau]);
+                D = __dadd_rn(D, __dmul_rn(diff, diff));
+                if ((om >> e) & 1u) {
+                    const unsigned bal = __ballot_sync(FULL, (pass >> e) & 1u);
+                    const int nt = min(W.thr[e], list_merge(W, e, bal, D, c0, lane, memb == nullptr));
+                    if (lane == 0) W.thr[e] = nt;
+                }
+            }
             __syncwarp();
 #pragma unroll
             for (int e = 0; e < ECAP; ++e)
@@ -309,11 +331,9 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, con
                     const double diff = __dsub_rn(q[e], cs[-e * tau]);
                     D = __dadd_rn(D, __dmul_rn(diff, diff));
                     // prefilter on the high word: D <= theta implies hi(D) <= hi(theta) (D >= 0)
-                    if (hi_word(D) <= thr[e]) {
-                        W.scr[e * 32 + lane] = D;
-                        pass |= 1u << e;
-                    }
+                    if (hi_word(D) <= thr[e]) pass |= 1u << e;
                 }
+                if (memb) pass &= ~memb[s];
                 if (__any_sync(FULL, pass != 0u)) flush(c0, pass);
             }
         } else {
@@ -327,12 +347,10 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, con
                     if (e < Eq) {
                         const double diff = __dsub_rn(q[e], cs[-e * tau]);
                         D = __dadd_rn(D, __dmul_rn(diff, diff));
-                        if (selected(e) && hi_word(D) <= thr[e]) {
-                            W.scr[e * 32 + lane] = D;
-                            pass |= 1u << e;
-                        }
+                        if (selected(e) && hi_word(D) <= thr[e]) pass |= 1u << e;
                     }
                 }
+                if (memb) pass &= ~memb[s];
                 if (__any_sync(FULL, pass != 0u)) flush(c0, pass);
             }
         }
@@ -388,7 +406,10 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnPa
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    KnnWarpSmem& W = reinterpret_cast<KnnWarpSmem*>(knn_smem + ((size_t)nx * sizeof(double) + 15) / 16 * 16)[warp];
+    unsigned char* wbase = knn_smem + ((size_t)nx * sizeof(double) + 15) / 16 * 16 + (size_t)warp * knn_warp_bytes(P.L);
+    KnnWarpSmem& W = *reinterpret_cast<KnnWarpSmem*>(wbase);
+    const int mw = knn_memb_words(P.L);
+    unsigned* memb = mw ? reinterpret_cast<unsigned*>(wbase + (sizeof(KnnWarpSmem) + 15) / 16 * 16) : nullptr;
     const double* xs = xs_pad + padl;
     unsigned mask = P.maskS;
     int Etop = P.Etop;
@@ -412,7 +433,7 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnPa
     }
     const int t0 = blockIdx.x * KNN_QPB + warp * KNN_QPW;
     const int t1 = min(nq, t0 + KNN_QPW);
-    if (t0 < t1) knn_warp<MODE, TAU1, FULLMASK>(P, W, qa, cb, t0, t1, ncand, mask, Etop, b, lane);
+    if (t0 < t1) knn_warp<MODE, TAU1, FULLMASK>(P, W, memb, mw, qa, cb, t0, t1, ncand, mask, Etop, b, lane);
 }
 
 // ------------------------------------------------------------------ S2 / S3 phase-1 skill
