@@ -158,10 +158,13 @@ constexpr int KNN_PADR = 32;
 // loff(e) + j, k = e + 2 entries) and the per-E prefilter bounds.
 __host__ __device__ constexpr int loff(int e) { return e * (e + 3) / 2; }
 constexpr int LIST_ENTRIES = loff(ECAP);  // 230
+constexpr int KNN_UMAX = 96;  // candidates of the union pre-pass (3 pseudo-chunks)
 struct KnnWarpSmem {
     double D[LIST_ENTRIES];
     int S[LIST_ENTRIES];
     int thr[ECAP];
+    unsigned ubits[64];   // union of the prefill candidates, as a bitmap over s (L <= 2048)
+    int ulist[KNN_UMAX];  // ... and as a sorted list
 };
 // Per-warp membership words memb[s] (bit e <=> candidate s was prefilled into list e): the
 // sweep drops those (candidate, E) pairs, which are already in the list with their exact
@@ -177,14 +180,14 @@ constexpr size_t knn_smem_bytes(int L, int tau) {
            (size_t)KNN_WARPS * knn_warp_bytes(L);
 }
 
-// Merge the lanes flagged in `bal` (this chunk's candidates that passed list e's prefilter;
-// distance `cand` in the lane's register, label c0 + lane) into list e (k entries sorted by
-// the (d2, s) lexicographic order of C4 / S:137). Candidates already in the list (prefilled
-// from the previous query, see knn_warp) are dropped first when no membership words exist.
-// Each list entry and each candidate then computes its rank in the merged sequence (one
-// broadcast per candidate) and the ones with rank < k are written to their slot. Returns the
-// hi word of the new k-th distance (+inf's while the list is not full).
-__device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, double cand, int c0, int lane,
+// Merge the lanes flagged in `bal` (candidates that passed list e's prefilter; distance `cand`
+// and label `sc` in the lane's registers, labels increasing with the lane) into list e (k
+// entries sorted by the (d2, s) lexicographic order of C4 / S:137). Candidates already in the
+// list are dropped first when no membership words exist (`dedup`). Each list entry and each
+// candidate then computes its rank in the merged sequence (one broadcast per candidate) and
+// the ones with rank < k are written to their slot. Returns the hi word of the new k-th
+// distance (+inf's while the list is not full).
+__device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, double cand, int sc, int lane,
                                           bool dedup) {
     const int k = e + 2;
     double* LD = W.D + loff(e);
@@ -193,8 +196,13 @@ __device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, d
     const double myD = isList ? LD[lane] : CUDART_INF;
     const int myS = isList ? LS[lane] : 0x7fffffff;
     if (dedup) {
-        const unsigned dl = (unsigned)(myS - c0);
-        bal &= ~__reduce_or_sync(FULL, (isList && dl < 32u) ? (1u << dl) : 0u);
+        unsigned b = bal;
+        do {
+            const int j = __ffs(b) - 1;
+            b &= b - 1;
+            const int sj = __shfl_sync(FULL, sc, j);  // all lanes (no short-circuit around it)
+            if (__any_sync(FULL, isList && myS == sj)) bal &= ~(1u << j);
+        } while (b);
         if (!bal) return hi_word(LD[k - 1]);
     }
     const bool isCand = (bal >> lane) & 1u;
@@ -205,15 +213,15 @@ __device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, d
         const int j = __ffs(b) - 1;
         b &= b - 1;
         const double Dj = __shfl_sync(FULL, cand, j);
-        const int sj = c0 + j;
+        const int sj = __shfl_sync(FULL, sc, j);
         const int pl = __popc(__ballot_sync(FULL, myD < Dj || (myD == Dj && myS < sj)));
         if (lane == j) nc += pl;
         nl += (Dj < myD || (Dj == myD && sj < myS)) ? 1 : 0;
-        nc += (Dj < cand || (Dj == cand && j < lane)) ? 1 : 0;
+        nc += (Dj < cand || (Dj == cand && sj < sc)) ? 1 : 0;
     } while (b);
     __syncwarp();
     if (isList && nl < k) { LD[nl] = myD; LS[nl] = myS; }
-    if (isCand && nc < k) { LD[nc] = cand; LS[nc] = c0 + lane; }
+    if (isCand && nc < k) { LD[nc] = cand; LS[nc] = sc; }
     __syncwarp();
     return hi_word(LD[k - 1]);
 }
@@ -251,6 +259,8 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
         if (memb) {
             for (int i = lane * 4; i < mw; i += 128)
                 *reinterpret_cast<uint4*>(memb + i) = make_uint4(0u, 0u, 0u, 0u);
+            W.ubits[lane] = 0u;
+            W.ubits[lane + 32] = 0u;
             __syncwarp();
         }
         for (int e = 0; e < Eq; ++e) {
@@ -282,7 +292,10 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
             if (lane < k) {
                 LD[rank] = all ? D : CUDART_INF;
                 LS[rank] = all ? c : 0x7fffffff;
-                if (all && memb) atomicOr(memb + c, 1u << e);
+                if (all && memb) {
+                    atomicOr(memb + c, 1u << e);
+                    atomicOr(&W.ubits[c >> 5], 1u << (c & 31));
+                }
             }
             __syncwarp();
             if (lane == 0) W.thr[e] = all ? min(THR_EMPTY, hi_word(LD[k - 1])) : THR_EMPTY;
@@ -295,22 +308,21 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
             q[e] = (e < Eq) ? qa[t - e * tau] : 0.0;
             thr[e] = (e < Eq) ? W.thr[e] : 0;
         }
-        // ---- sweep over the candidates in increasing s
-        auto flush = [&](int c0, unsigned pass) {
+        // ---- candidate chunks: lane holds candidate s (distance D_E for E = 1..Eq)
+        auto flush = [&](int s, unsigned pass) {
             // list merges for every E that had a passing lane in this chunk; the candidate
             // distances are recomputed (same operation sequence) up to the largest such E
             unsigned om = __reduce_or_sync(FULL, pass);
-            const int s = c0 + lane;
             const double* cs = cb + s;
             const double* qt = qa + t;
-            double D = (s < ncand && !(excl && s == t)) ? 0.0 : CUDART_INF;
+            double D = (s >= 0 && s < ncand && !(excl && s == t)) ? 0.0 : CUDART_INF;
             const int elast = 31 - __clz(om);
             for (int e = 0; e <= elast; ++e) {
                 const double diff = __dsub_rn(qt[-e * tau], cs[-e * tau]);
                 D = __dadd_rn(D, __dmul_rn(diff, diff));
                 if ((om >> e) & 1u) {
                     const unsigned bal = __ballot_sync(FULL, (pass >> e) & 1u);
-                    const int nt = min(W.thr[e], list_merge(W, e, bal, D, c0, lane, memb == nullptr));
+                    const int nt = min(W.thr[e], list_merge(W, e, bal, D, s, lane, memb == nullptr));
                     if (lane == 0) W.thr[e] = nt;
                 }
             }
@@ -319,13 +331,12 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
             for (int e = 0; e < ECAP; ++e)
                 if (e < Eq) thr[e] = W.thr[e];
         };
-        if (FULLMASK && Eq == ECAP) {
-            // main path: every E = 1..ECAP kept, fully unrolled without per-E tests
-            for (int c0 = 0; c0 < ncand; c0 += 32) {
-                const int s = c0 + lane;
-                const double* cs = cb + s;  // padded: cs[-e*tau] is addressable for e < ECAP
-                double D = (s < ncand && !(excl && s == t)) ? 0.0 : CUDART_INF;
-                unsigned pass = 0u;
+        auto chunk = [&](int s) {
+            const double* cs = cb + s;  // padded: cs[-e*tau] is addressable for e < ECAP, s >= 0
+            double D = (s < ncand && !(excl && s == t)) ? 0.0 : CUDART_INF;
+            unsigned pass = 0u;
+            if (FULLMASK && Eq == ECAP) {
+                // main path: every E = 1..ECAP kept, fully unrolled without per-E tests
 #pragma unroll
                 for (int e = 0; e < ECAP; ++e) {
                     const double diff = __dsub_rn(q[e], cs[-e * tau]);
@@ -333,15 +344,7 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
                     // prefilter on the high word: D <= theta implies hi(D) <= hi(theta) (D >= 0)
                     if (hi_word(D) <= thr[e]) pass |= 1u << e;
                 }
-                if (memb) pass &= ~memb[s];
-                if (__any_sync(FULL, pass != 0u)) flush(c0, pass);
-            }
-        } else {
-            for (int c0 = 0; c0 < ncand; c0 += 32) {
-                const int s = c0 + lane;
-                const double* cs = cb + s;
-                double D = (s < ncand && !(excl && s == t)) ? 0.0 : CUDART_INF;
-                unsigned pass = 0u;
+            } else {
 #pragma unroll
                 for (int e = 0; e < ECAP; ++e) {
                     if (e < Eq) {
@@ -350,10 +353,50 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
                         if (selected(e) && hi_word(D) <= thr[e]) pass |= 1u << e;
                     }
                 }
-                if (memb) pass &= ~memb[s];
-                if (__any_sync(FULL, pass != 0u)) flush(c0, pass);
             }
+            if (memb) pass &= ~memb[s];
+            if (__any_sync(FULL, pass != 0u)) flush(s, pass);
+        };
+        if (memb) {
+            // ---- union pre-pass: every prefill candidate (the union over E of the successor
+            // sets, up to KNN_UMAX, in increasing s) is tested against every list now, then
+            // marked as done for all E so the sweep skips it. Near neighbours thus meet the
+            // lists early, which leaves few merges for the sweep.
+            const unsigned w0 = W.ubits[lane], w1 = W.ubits[lane + 32];
+            const int cnt = __popc(w0), cnt1 = __popc(w1);
+            int off = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(FULL, off, o);
+                if (lane >= o) off += v;
+            }
+            const int tot0 = __shfl_sync(FULL, off, 31);
+            off -= cnt;
+            int off1 = cnt1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(FULL, off1, o);
+                if (lane >= o) off1 += v;
+            }
+            const int nU = min(KNN_UMAX, tot0 + __shfl_sync(FULL, off1, 31));
+            off1 += tot0 - cnt1;
+            for (unsigned w = w0; w; w &= w - 1, ++off)
+                if (off < KNN_UMAX) W.ulist[off] = (lane << 5) + __ffs(w) - 1;
+            for (unsigned w = w1; w; w &= w - 1, ++off1)
+                if (off1 < KNN_UMAX) W.ulist[off1] = ((lane + 32) << 5) + __ffs(w) - 1;
+            __syncwarp();
+            for (int g = 0; g < nU; g += 32) {
+                const bool in = g + lane < nU;
+                const int su = in ? W.ulist[g + lane] : 0;
+                // lanes past the union carry s = 0 with D poisoned through the ncand test
+                chunk(in ? su : ncand);
+            }
+            __syncwarp();
+            for (int g = lane; g < nU; g += 32) memb[W.ulist[g]] = 0xffffffffu;
+            __syncwarp();
         }
+        // ---- sweep over all candidates in increasing s
+        for (int c0 = 0; c0 < ncand; c0 += 32) chunk(c0 + lane);
         // ---- finalise every selected E of this query
         for (int e = 0; e < Eq; ++e) {
             if (!selected(e)) continue;
