@@ -22,7 +22,7 @@ constexpr int ECAP = 20;            // largest E (k = E + 1 <= 21 <= 32 lanes)
 constexpr int TILE_J = 32;          // targets per lookup tile (one per lane)
 constexpr int KNN_WARPS = 4;        // warps per knn CTA
 constexpr int KNN_MIN_CTAS = 4;     // resident CTAs per SM the register budget must allow
-constexpr int KNN_QPW = 16;         // consecutive queries per warp
+constexpr int KNN_QPW = 64;         // consecutive queries per warp
 constexpr int KNN_QPB = KNN_WARPS * KNN_QPW;
 constexpr int LOOKUP_WARPS = 16;    // warps per lookup CTA (one library each)
 constexpr unsigned FULL = 0xffffffffu;

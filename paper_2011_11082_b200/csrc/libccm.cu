@@ -100,7 +100,7 @@ void table_layout(int L, int tau, int Tp, int64_t offE[ECAP + 2], int64_t* T_lib
 }
 
 constexpr int SIMPLEX_SLOTS = 2048;   // series per phase-1 block
-constexpr int CCM_B = 4 * LOOKUP_WARPS;   // libraries per phase-2 block (4 per lookup warp)
+constexpr int CCM_B = 16 * LOOKUP_WARPS;  // libraries per phase-2 block (16 per lookup warp)
 constexpr int LOOKUP_SMEM_MAX = 227 * 1024;
 
 inline int64_t np_max(int N) { return (int64_t)(N + TILE_J - 1) / TILE_J * TILE_J + (int64_t)TILE_J * ECAP; }
