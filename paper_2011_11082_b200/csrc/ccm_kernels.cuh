@@ -405,10 +405,10 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
             const double d2 = lane < k ? W.D[loff(e) + lane] : CUDART_INF;
             const int sl = lane < k ? W.S[loff(e) + lane] : 0;
             if (MODE == MODE_CCM) {
-                const double w = simplex_weight<false>(d2, k, lane);
+                // {s + Tp, fp32 distance}; weights_kernel turns the distance into the weight
                 const int kp = kpad(k);
                 if (lane < kp) {
-                    uint2 ent = lane < k ? make_uint2((unsigned)(sl + P.Tp), __float_as_uint((float)w))
+                    uint2 ent = lane < k ? make_uint2((unsigned)(sl + P.Tp), __float_as_uint((float)sqrt(d2)))
                                          : make_uint2(0u, 0u);
                     P.tables[(int64_t)b * P.T_lib + P.offE[e + 1] + (int64_t)row * kp + lane] = ent;
                 }
@@ -477,6 +477,46 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnPa
     const int t0 = blockIdx.x * KNN_QPB + warp * KNN_QPW;
     const int t1 = min(nq, t0 + KNN_QPW);
     if (t0 < t1) knn_warp<MODE, TAU1, FULLMASK>(P, W, memb, mw, qa, cb, t0, t1, ncand, mask, Etop, b, lane);
+}
+
+// Weights of the phase-2 tables (S8, C5), one thread per table row: the kNN kernel
+// stored fp32(sqrt(d2)) (zero exactly when d2 is zero: the smallest nonzero d2 of fp32 data is
+// 2^-298, whose root 2^-149 is representable), here u_j = exp(-d_j/d_1) if d_1 > 0 else
+// [d_j == 0], floored at 1e-6 and normalised; stored as fp32 (rows of all selected E of the
+// block's libraries; row r of E starts at offE[E] + r * kpad(E+1) of library b's table).
+struct WeightParams {
+    uint2* tables;
+    int64_t T_lib;
+    int64_t offE[ECAP + 2];
+    int rowStart[ECAP + 2];  // cumulative row counts over the selected E (rowStart[ECAP+1] = total)
+    int nlib;
+};
+__global__ void weights_kernel(WeightParams P) {
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int total = P.rowStart[ECAP + 1];
+    if (gid >= (int64_t)total * P.nlib) return;
+    const int b = (int)(gid / total);
+    const int r = (int)(gid - (int64_t)b * total);
+    int E = 1;
+    while (E <= ECAP && r >= P.rowStart[E + 1]) ++E;
+    const int k = E + 1, kp = kpad(k);
+    uint2* row = P.tables + (int64_t)b * P.T_lib + P.offE[E] + (int64_t)(r - P.rowStart[E]) * kp;
+    float d[ECAP + 1], u[ECAP + 1];
+    float sum = 0.f;
+    const float d1 = __uint_as_float(row[0].y);
+#pragma unroll
+    for (int j = 0; j < ECAP + 1; ++j) {
+        if (j < k) {
+            d[j] = __uint_as_float(row[j].y);
+            float v = d1 > 0.f ? __expf(-__fdividef(d[j], d1)) : (d[j] == 0.f ? 1.f : 0.f);
+            v = fmaxf(v, 1e-6f);
+            u[j] = v;
+            sum += v;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < ECAP + 1; ++j)
+        if (j < k) row[j].y = __float_as_uint(u[j] / sum);
 }
 
 // ------------------------------------------------------------------ S2 / S3 phase-1 skill

@@ -394,6 +394,20 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int3
         memcpy(P.offE, offE, sizeof(offE));
         st = launch_knn<MODE_CCM>(P, L - Tp, nb, cs);
         if (st != EDM_OK) return st;
+        {
+            WeightParams WP{};
+            WP.tables = W.tables; WP.T_lib = T_lib; WP.nlib = nb;
+            memcpy(WP.offE, offE, sizeof(offE));
+            int acc = 0;
+            for (int E = 1; E <= ECAP + 1; ++E) {
+                WP.rowStart[E] = acc;
+                if (E <= ECAP && ((maskS >> E) & 1u)) acc += (int)std::max<int64_t>(n_rows(L, E, tau, Tp), 0);
+            }
+            WP.rowStart[0] = 0;
+            const int64_t nthr = (int64_t)acc * nb;
+            PROF_LAUNCH(EDM_PROF_CCM_KNN, cs, weights_kernel<<<(unsigned)((nthr + 255) / 256), 256, 0, cs>>>(WP));
+            LAUNCH_CHECK("weights_kernel");
+        }
         LookupParams Q{};
         Q.Yp = W.Yp; Q.Np = Np; Q.colmap = W.colmap;
         Q.tileE = (mode == EDM_E_TARGET) ? W.tileE : nullptr;
