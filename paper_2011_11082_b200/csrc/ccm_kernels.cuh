@@ -116,13 +116,20 @@ struct KnnParams {
     uint2* tables;
     int64_t T_lib;
     int64_t offE[ECAP + 2];
-    // MODE_SIMPLEX output: pred[(b * ECAP + E-1) * LQ + t] (fp64 forecast of target point t)
-    double* pred;
-    int LQ;
+    // MODE_SIMPLEX output: the sorted list of target point t at E, entry j at
+    // b * S_slot + offS[E] + t * (E+1) + j: squared distance sd2 (fp64) and library index ss
+    double* sd2;
+    int* ss;
+    int64_t S_slot;
+    int64_t offS[ECAP + 2];
     // MODE_EMBED output (rows t - (E-1)tau, k columns)
     int* out_idx;
     float* out_dist;
     float* out_w;
+};
+
+struct KnnOffsets {
+    int64_t offS[ECAP + 2];
 };
 
 __device__ __forceinline__ int hi_word(double d) { return __double2hiint(d); }
@@ -419,12 +426,12 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
                     P.out_dist[(int64_t)row * k + lane] = (float)sqrt(d2);
                     if (P.out_w) P.out_w[(int64_t)row * k + lane] = (float)w;
                 }
-            } else {  // MODE_SIMPLEX: forecast one step ahead, yhat = sum_k w_k lib[s_k + 1]
-                const double w = simplex_weight<true>(d2, k, lane);
-                const double prod = lane < k ? __dmul_rn(w, cb[sl + 1]) : 0.0;
-                double acc = 0.0;
-                for (int j = 0; j < k; ++j) acc = __dadd_rn(acc, __shfl_sync(FULL, prod, j));
-                if (lane == 0) P.pred[((int64_t)b * ECAP + e) * P.LQ + t] = acc;
+            } else {  // MODE_SIMPLEX: the (d2, s) list goes to forecast_kernel
+                if (lane < k) {
+                    const int64_t o = (int64_t)b * P.S_slot + P.offS[e + 1] + (int64_t)t * k + lane;
+                    P.sd2[o] = d2;
+                    P.ss[o] = sl;
+                }
             }
         }
         prevEq = Eq;
@@ -520,6 +527,45 @@ __global__ void weights_kernel(WeightParams P) {
 }
 
 // ------------------------------------------------------------------ S2 / S3 phase-1 skill
+// Phase-1 forecasts, one thread per (series slot, E, target point t): the weights of C5 and
+// yhat(t) = sum_k w_k lib[s_k + 1] (Alg. 1 line 7; one step ahead) in fp64
+// with the oracle's exact operation order (sequential sums, separately rounded ops), from the
+// (d2, s) lists of knn_kernel<SIMPLEX>. pred[(b * ECAP + E-1) * LQ + t].
+__global__ void forecast_kernel(const double* __restrict__ sd2, const int* __restrict__ ss, int64_t S_slot,
+                                KnnOffsets O, const float* __restrict__ X, int64_t ldx, int L, int tau, unsigned mask,
+                                int nslots, int LQ, double* __restrict__ pred) {
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int nq = (L - (L + 1) / 2) - 1;
+    if (gid >= (int64_t)nslots * ECAP * nq) return;
+    const int t = (int)(gid % nq);
+    const int e = (int)((gid / nq) % ECAP);
+    const int b = (int)(gid / ((int64_t)nq * ECAP));
+    if (!((mask >> (e + 1)) & 1u) || t < e * tau) return;
+    const int k = e + 2;
+    const int64_t o = (int64_t)b * S_slot + O.offS[e + 1] + (int64_t)t * k;
+    const float* lib = X + (int64_t)b * ldx;
+    double u[ECAP + 1];
+    const double d1 = sqrt(sd2[o]);
+    double sum = 0.0;
+#pragma unroll
+    for (int j = 0; j < ECAP + 1; ++j) {
+        if (j < k) {
+            const double d = sqrt(sd2[o + j]);
+            double v;
+            if (d1 > 0.0) v = exp(__ddiv_rn(-d, d1));
+            else v = (d == 0.0) ? 1.0 : 0.0;
+            if (v < 1e-6) v = 1e-6;
+            u[j] = v;
+            sum = __dadd_rn(sum, v);
+        }
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < ECAP + 1; ++j)
+        if (j < k) acc = __dadd_rn(acc, __dmul_rn(__ddiv_rn(u[j], sum), (double)lib[ss[o + j] + 1]));
+    pred[((int64_t)b * ECAP + e) * LQ + t] = acc;
+}
+
 // rho(E) of series slot b: two-pass fp64 Pearson of (pred[t], tgt[t+1]) over the query rows
 // t in [(E-1)tau, Ltgt-2], in the oracle's order (C7); NaN if infeasible or constant.
 __global__ void simplex_rho_kernel(const float* __restrict__ X, int64_t ldx, const double* __restrict__ pred,

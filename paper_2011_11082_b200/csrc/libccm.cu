@@ -99,7 +99,7 @@ void table_layout(int L, int tau, int Tp, int64_t offE[ECAP + 2], int64_t* T_lib
     *T_lib = off;
 }
 
-constexpr int SIMPLEX_SLOTS = 2048;   // series per phase-1 block
+constexpr int SIMPLEX_SLOTS = 1024;   // series per phase-1 block
 constexpr int CCM_B = 16 * LOOKUP_WARPS;  // libraries per phase-2 block (16 per lookup warp)
 constexpr int LOOKUP_SMEM_MAX = 227 * 1024;
 
@@ -109,18 +109,32 @@ struct SimplexWs {
     float* Xs;      // [SB][L]
     double* pred;   // [SB][ECAP][LQ]
     double* rho;    // [SB][E_max]
+    double* sd2;    // [SB][S_slot] sorted lists (squared distances)
+    int* ss;        // [SB][S_slot] sorted lists (library indices)
+    int64_t S_slot;
+    int64_t offS[ECAP + 2];
     size_t bytes;
 };
 
+// Lists of every (E, target point): entries per slot = sum_E (E+1) * LQ.
 SimplexWs simplex_ws(void* base, int N, int L, int E_max) {
     SimplexWs w{};
     const int SB = std::min(N, SIMPLEX_SLOTS);
     const int LQ = std::max(L / 2, 1);
+    int64_t acc = 0;
+    w.offS[0] = 0;
+    for (int E = 1; E <= ECAP + 1; ++E) {
+        w.offS[E] = acc;
+        if (E <= ECAP) acc += (int64_t)(E + 1) * LQ;
+    }
+    w.S_slot = acc;
     size_t off = 0;
     char* b = (char*)base;
     w.Xs = (float*)(b + off);   off += align_up((size_t)SB * L * sizeof(float));
     w.pred = (double*)(b + off); off += align_up((size_t)SB * ECAP * LQ * sizeof(double));
     w.rho = (double*)(b + off);  off += align_up((size_t)SB * std::max(E_max, 1) * sizeof(double));
+    w.sd2 = (double*)(b + off);  off += align_up((size_t)SB * acc * sizeof(double));
+    w.ss = (int*)(b + off);      off += align_up((size_t)SB * acc * sizeof(int));
     w.bytes = off;
     return w;
 }
@@ -280,9 +294,21 @@ edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int
         if (Etop > 0) {
             KnnParams P{};
             P.X = W.Xs; P.ldx = L; P.L = L; P.tau = tau; P.Tp = 1; P.excl = 0;
-            P.maskS = mask; P.Etop = Etop; P.pred = W.pred; P.LQ = LQ;
+            P.maskS = mask; P.Etop = Etop;
+            P.sd2 = W.sd2; P.ss = W.ss; P.S_slot = W.S_slot;
+            memcpy(P.offS, W.offS, sizeof(W.offS));
             st = launch_knn<MODE_SIMPLEX>(P, std::max(Ltgt - 1, 1), nb, cs);
             if (st != EDM_OK) return st;
+            KnnOffsets O;
+            memcpy(O.offS, W.offS, sizeof(W.offS));
+            const int nq = std::max(Ltgt - 1, 0);
+            const int64_t nthr = (int64_t)nb * ECAP * nq;
+            if (nthr > 0) {
+                PROF_LAUNCH(EDM_PROF_SIMPLEX_KNN, cs,
+                            forecast_kernel<<<(unsigned)((nthr + 127) / 128), 128, 0, cs>>>(W.sd2, W.ss, W.S_slot, O, W.Xs, L, L,
+                                                                                          tau, mask, nb, LQ, W.pred));
+                LAUNCH_CHECK("forecast_kernel");
+            }
         }
         const int nthr = nb * E_max;
         PROF_LAUNCH(EDM_PROF_SIMPLEX_RHO, cs, simplex_rho_kernel<<<(nthr + 127) / 128, 128, 0, cs>>>(W.Xs, L, W.pred, LQ, L, tau, E_max, nb, W.rho));
