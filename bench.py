@@ -300,6 +300,14 @@ def main():
     phases = np.zeros(4)
     for e in evs:
         phases += [e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]), e[3].elapsed_time(e[4])]
+    per_rank = [None] * world
+    mine = {"rank": rank, "ms": ms_local, "simplex": phases[0] / args.steps, "allgather_E": phases[1] / args.steps,
+            "ccm": phases[2] / args.steps, "gather_rho": phases[3] / args.steps,
+            "kernels": {k: round(v[0] / args.steps, 1) for k, v in prof.items()}}
+    if world > 1:
+        dist.all_gather_object(per_rank, mine)
+    else:
+        per_rank = [mine]
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev if world > 1 else "cpu")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -414,6 +422,7 @@ def main():
             "phase_ms_per_step": {"simplex": phases[0] / args.steps, "allgather_E": phases[1] / args.steps,
                                   "ccm": phases[2] / args.steps, "gather_rho": phases[3] / args.steps},
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+            "per_rank_ms_per_step": per_rank if world > 1 else None,
             "E_hist": hist, "k_bar": float((E_host + 1).mean()),
             "roofline": roofline_main, other_key: roofline_other,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,

@@ -202,6 +202,14 @@ __device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, d
     const bool isList = lane < k;
     const double myD = isList ? LD[lane] : CUDART_INF;
     const int myS = isList ? LS[lane] : 0x7fffffff;
+    {
+        // exact test against the current k-th key: drops hi-word false positives and, above
+        // all, floods of exact ties (e.g. a constant series, where every D is 0)
+        const double thD = LD[k - 1];
+        const int thS = LS[k - 1];
+        bal &= __ballot_sync(FULL, cand < thD || (cand == thD && sc < thS));
+        if (!bal) return hi_word(thD);
+    }
     if (dedup) {
         unsigned b = bal;
         do {
