@@ -213,3 +213,39 @@ def test_c3_full_size_sampled():
         pick = [0, 17, 63]
         ref = np.concatenate([O.ccm_rows(data, optE, 1, 1, 0, True, r0 + p, r0 + p + 1) for p in pick])
         assert_rho_close(rows[pick], ref)
+
+
+def test_c4_full_size_sampled():
+    """c4 (101,729 x 1,450, the north_star's 8-GPU target) at full size: optE on sampled
+    series and rho on every target of sampled library rows (one 256-library block)."""
+    data = synth.make_config("c4")
+    L, N = data.shape
+    d = dev(data)
+    rng = np.random.default_rng(11)
+    ss = np.sort(rng.choice(N, 24, replace=False))
+    optE = libccm.simplex_optimal_E(d, 20).cpu().numpy()
+    for s in ss:
+        e, _, _ = O.simplex(data[:, s].astype(np.float64), 20)
+        assert e == optE[s], (s, e, optE[s])
+    r0 = 50_000
+    rows = libccm.ccm_all_pairs(d, dev(optE, torch.int32), 1, 1, "target", True, r0, r0 + 256).cpu().numpy()
+    pick = [5, 130, 255]
+    ref = np.concatenate([O.ccm_rows(data, optE, 1, 1, 0, True, r0 + p, r0 + p + 1) for p in pick])
+    assert_rho_close(rows[pick], ref)
+
+
+def test_c5_long_series_sampled():
+    """c5 shape (L = 10,000, E up to 20; kNN/distance-dominated regime): full-length series,
+    a sample of 64 series x 64 sampled rows' worth of targets, incl. the forced-E variant
+    E[j] = 1 + (j mod 20) that exercises all 20 tables."""
+    data = synth.make_config("c5", N=64)
+    L, N = data.shape
+    d = dev(data)
+    optE = libccm.simplex_optimal_E(d, 20, 1, 0, 8).cpu().numpy()
+    for s in range(8):
+        e, _, _ = O.simplex(data[:, s].astype(np.float64), 20)
+        assert e == optE[s]
+    forced = (1 + np.arange(N) % 20).astype(np.int32)
+    rows = libccm.ccm_all_pairs(d, dev(forced, torch.int32), 1, 1, "target", True, 3, 5).cpu().numpy()
+    ref = O.ccm_rows(data, forced, 1, 1, 0, True, 3, 5)
+    assert_rho_close(rows, ref)
