@@ -505,6 +505,7 @@ struct WeightParams {
     int64_t offE[ECAP + 2];
     int rowStart[ECAP + 2];  // cumulative row counts over the selected E (rowStart[ECAP+1] = total)
     int nlib;
+    const int* slotE;        // library mode: only the rows of E = slotE[b] exist
 };
 __global__ void weights_kernel(WeightParams P) {
     const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -514,6 +515,7 @@ __global__ void weights_kernel(WeightParams P) {
     const int r = (int)(gid - (int64_t)b * total);
     int E = 1;
     while (E <= ECAP && r >= P.rowStart[E + 1]) ++E;
+    if (P.slotE && P.slotE[b] != E) return;
     const int k = E + 1, kp = kpad(k);
     uint2* row = P.tables + (int64_t)b * P.T_lib + P.offE[E] + (int64_t)(r - P.rowStart[E]) * kp;
     float d[ECAP + 1], u[ECAP + 1];

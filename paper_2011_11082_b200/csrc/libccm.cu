@@ -423,6 +423,7 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int3
         {
             WeightParams WP{};
             WP.tables = W.tables; WP.T_lib = T_lib; WP.nlib = nb;
+            WP.slotE = (mode == EDM_E_LIBRARY) ? W.slotE + r0 : nullptr;
             memcpy(WP.offE, offE, sizeof(offE));
             int acc = 0;
             for (int E = 1; E <= ECAP + 1; ++E) {
