@@ -158,7 +158,13 @@ __device__ __forceinline__ double simplex_weight(double d2, int k, int lane) {
 }
 
 constexpr double PAD_VALUE = 1e300;   // (q - PAD)^2 = +inf: out-of-range coordinates poison D
-constexpr int THR_EMPTY = 0x7fefffff; // hi word of the largest finite double (rejects +inf)
+constexpr float THR_EMPTY = 3.402823466e38f;  // FLT_MAX: an empty list admits every finite candidate
+// fp32 prefilter bound of a fp64 list distance D: the sweep accumulates D in fp32, whose
+// relative error is below (E+3) 2^-24 < 2^-18 for E <= 20 (fp32 inputs, no overflow), so any
+// candidate with exact D_E <= D has fp32 D_E <= bound(D); the merge then decides exactly in fp64.
+__device__ __forceinline__ float prefilter_bound(double D) {
+    return D < 1e300 ? fminf(THR_EMPTY, __double2float_ru(__dmul_ru(D, 1.0 + 0x1p-18))) : THR_EMPTY;
+}
 __host__ __device__ constexpr int knn_padl(int tau) { return (ECAP - 1) * tau; }
 constexpr int KNN_PADR = 32;
 // Per-warp shared-memory state: the sorted top-(E+1) list of every E (entry j of list e at
@@ -169,7 +175,7 @@ constexpr int KNN_UMAX = 96;  // candidates of the union pre-pass (3 pseudo-chun
 struct KnnWarpSmem {
     double D[LIST_ENTRIES];
     int S[LIST_ENTRIES];
-    int thr[ECAP];
+    float thr[ECAP];
     unsigned ubits[64];   // union of the prefill candidates, as a bitmap over s (L <= 2048)
     int ulist[KNN_UMAX];  // ... and as a sorted list
 };
@@ -184,7 +190,7 @@ __host__ __device__ constexpr size_t knn_warp_bytes(int L) {
 }
 constexpr size_t knn_smem_bytes(int L, int tau) {
     return ((size_t)(knn_padl(tau) + L + KNN_PADR) * sizeof(double) + 15) / 16 * 16 +
-           (size_t)KNN_WARPS * knn_warp_bytes(L);
+           (size_t)KNN_WARPS * knn_warp_bytes(L) + (size_t)(knn_padl(tau) + L + KNN_PADR) * sizeof(float);
 }
 
 // Merge the lanes flagged in `bal` (candidates that passed list e's prefilter; distance `cand`
@@ -194,7 +200,7 @@ constexpr size_t knn_smem_bytes(int L, int tau) {
 // candidate then computes its rank in the merged sequence (one broadcast per candidate) and
 // the ones with rank < k are written to their slot. Returns the hi word of the new k-th
 // distance (+inf's while the list is not full).
-__device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, double cand, int sc, int lane,
+__device__ __forceinline__ double list_merge(KnnWarpSmem& W, int e, unsigned bal, double cand, int sc, int lane,
                                           bool dedup) {
     const int k = e + 2;
     double* LD = W.D + loff(e);
@@ -208,7 +214,7 @@ __device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, d
         const double thD = LD[k - 1];
         const int thS = LS[k - 1];
         bal &= __ballot_sync(FULL, cand < thD || (cand == thD && sc < thS));
-        if (!bal) return hi_word(thD);
+        if (!bal) return thD;
     }
     if (dedup) {
         unsigned b = bal;
@@ -218,7 +224,7 @@ __device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, d
             const int sj = __shfl_sync(FULL, sc, j);  // all lanes (no short-circuit around it)
             if (__any_sync(FULL, isList && myS == sj)) bal &= ~(1u << j);
         } while (b);
-        if (!bal) return hi_word(LD[k - 1]);
+        if (!bal) return LD[k - 1];
     }
     const bool isCand = (bal >> lane) & 1u;
     int nl = lane;  // rank of my list entry
@@ -238,7 +244,7 @@ __device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, d
     if (isList && nl < k) { LD[nl] = myD; LS[nl] = myS; }
     if (isCand && nc < k) { LD[nc] = cand; LS[nc] = sc; }
     __syncwarp();
-    return hi_word(LD[k - 1]);
+    return LD[k - 1];
 }
 
 // One warp, queries t = t_begin .. t_end-1 in order. For each query: D_E(t, s) for E = 1..Eq
@@ -259,8 +265,9 @@ __device__ __forceinline__ int list_merge(KnnWarpSmem& W, int e, unsigned bal, d
 // result: the final list is the k smallest keys over all candidates either way.
 template <int MODE, bool TAU1, bool FULLMASK>
 __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, unsigned* memb, int mw,
-                                         const double* __restrict__ qa,
-                                         const double* __restrict__ cb, int t_begin, int t_end, int ncand,
+                                         const double* __restrict__ qa, const double* __restrict__ cb,
+                                         const float* __restrict__ qaf, const float* __restrict__ cbf,
+                                         int t_begin, int t_end, int ncand,
                                          unsigned mask, int Etop, int b, int lane) {
     const int tau = TAU1 ? 1 : P.tau;
     const bool excl = (MODE != MODE_SIMPLEX) && P.excl;
@@ -313,14 +320,14 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
                 }
             }
             __syncwarp();
-            if (lane == 0) W.thr[e] = all ? min(THR_EMPTY, hi_word(LD[k - 1])) : THR_EMPTY;
+            if (lane == 0) W.thr[e] = all ? prefilter_bound(LD[k - 1]) : THR_EMPTY;
         }
         __syncwarp();
-        double q[ECAP];
-        int thr[ECAP];
+        float q[ECAP];
+        float thr[ECAP];
 #pragma unroll
         for (int e = 0; e < ECAP; ++e) {
-            q[e] = (e < Eq) ? qa[t - e * tau] : 0.0;
+            q[e] = (e < Eq) ? qaf[t - e * tau] : 0.f;
             thr[e] = (e < Eq) ? W.thr[e] : 0;
         }
         // ---- candidate chunks: lane holds candidate s (distance D_E for E = 1..Eq)
@@ -337,7 +344,7 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
                 D = __dadd_rn(D, __dmul_rn(diff, diff));
                 if ((om >> e) & 1u) {
                     const unsigned bal = __ballot_sync(FULL, (pass >> e) & 1u);
-                    const int nt = min(W.thr[e], list_merge(W, e, bal, D, s, lane, memb == nullptr));
+                    const float nt = fminf(W.thr[e], prefilter_bound(list_merge(W, e, bal, D, s, lane, memb == nullptr)));
                     if (lane == 0) W.thr[e] = nt;
                 }
             }
@@ -347,25 +354,25 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
                 if (e < Eq) thr[e] = W.thr[e];
         };
         auto chunk = [&](int s) {
-            const double* cs = cb + s;  // padded: cs[-e*tau] is addressable for e < ECAP, s >= 0
-            double D = (s < ncand && !(excl && s == t)) ? 0.0 : CUDART_INF;
+            // fp32 prefilter sweep (the exact fp64 distances are recomputed in the flush)
+            const float* cs = cbf + s;  // padded: cs[-e*tau] is addressable for e < ECAP, s >= 0
+            float D = (s < ncand && !(excl && s == t)) ? 0.f : CUDART_INF_F;
             unsigned pass = 0u;
             if (FULLMASK && Eq == ECAP) {
                 // main path: every E = 1..ECAP kept, fully unrolled without per-E tests
 #pragma unroll
                 for (int e = 0; e < ECAP; ++e) {
-                    const double diff = __dsub_rn(q[e], cs[-e * tau]);
-                    D = __dadd_rn(D, __dmul_rn(diff, diff));
-                    // prefilter on the high word: D <= theta implies hi(D) <= hi(theta) (D >= 0)
-                    if (hi_word(D) <= thr[e]) pass |= 1u << e;
+                    const float diff = q[e] - cs[-e * tau];
+                    D = fmaf(diff, diff, D);
+                    if (D <= thr[e]) pass |= 1u << e;
                 }
             } else {
 #pragma unroll
                 for (int e = 0; e < ECAP; ++e) {
                     if (e < Eq) {
-                        const double diff = __dsub_rn(q[e], cs[-e * tau]);
-                        D = __dadd_rn(D, __dmul_rn(diff, diff));
-                        if (selected(e) && hi_word(D) <= thr[e]) pass |= 1u << e;
+                        const float diff = q[e] - cs[-e * tau];
+                        D = fmaf(diff, diff, D);
+                        if (selected(e) && D <= thr[e]) pass |= 1u << e;
                     }
                 }
             }
@@ -458,9 +465,13 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnPa
     const float* xg = P.X + (int64_t)row * P.ldx;
     const int padl = knn_padl(P.tau);
     const int nx = padl + P.L + KNN_PADR;
+    float* xf_pad = reinterpret_cast<float*>(knn_smem + ((size_t)nx * sizeof(double) + 15) / 16 * 16 +
+                                             (size_t)KNN_WARPS * knn_warp_bytes(P.L));
     for (int i = threadIdx.x; i < nx; i += blockDim.x) {
         const int t = i - padl;
-        xs_pad[i] = (t >= 0 && t < P.L) ? (double)xg[t] : PAD_VALUE;
+        const float v = (t >= 0 && t < P.L) ? xg[t] : 1e30f;  // (q - 1e30)^2 = +inf in fp32
+        xs_pad[i] = (t >= 0 && t < P.L) ? (double)v : PAD_VALUE;
+        xf_pad[i] = v;
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -478,20 +489,26 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnPa
     }
     const double* qa;
     const double* cb;
+    const float* xf = xf_pad + padl;
+    const float* qaf;
+    const float* cbf;
     int nq, ncand;
     if (MODE == MODE_SIMPLEX) {
         const int Llib = (P.L + 1) / 2;   // library = first ceil(L/2) samples
         cb = xs;
         qa = xs + Llib;
+        cbf = xf;
+        qaf = xf + Llib;
         nq = (P.L - Llib) - 1;            // target points t with t+1 inside the target half
         ncand = Llib - 1;                 // library points s with s+1 inside the library half
     } else {
         qa = cb = xs;
+        qaf = cbf = xf;
         nq = ncand = P.L - P.Tp;          // P_1 = [0, L-1-Tp]; per-E lower bound (E-1)tau
     }
     const int t0 = blockIdx.x * KNN_QPB + warp * KNN_QPW;
     const int t1 = min(nq, t0 + KNN_QPW);
-    if (t0 < t1) knn_warp<MODE, TAU1, FULLMASK>(P, W, memb, mw, qa, cb, t0, t1, ncand, mask, Etop, b, lane);
+    if (t0 < t1) knn_warp<MODE, TAU1, FULLMASK>(P, W, memb, mw, qa, cb, qaf, cbf, t0, t1, ncand, mask, Etop, b, lane);
 }
 
 // Weights of the phase-2 tables (S8, C5), one thread per table row: the kNN kernel
