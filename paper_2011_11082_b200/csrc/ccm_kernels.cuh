@@ -21,7 +21,7 @@ namespace ccm {
 constexpr int ECAP = 20;            // largest E (k = E + 1 <= 21 <= 32 lanes)
 constexpr int TILE_J = 32;          // targets per lookup tile (one per lane)
 constexpr int KNN_WARPS = 4;        // warps per knn CTA
-constexpr int KNN_MIN_CTAS = 4;     // resident CTAs per SM the register budget must allow
+constexpr int KNN_MIN_CTAS = 5;     // resident CTAs per SM the register budget must allow
 constexpr int KNN_QPW = 64;         // consecutive queries per warp
 constexpr int KNN_QPB = KNN_WARPS * KNN_QPW;
 constexpr int LOOKUP_WARPS = 16;    // warps per lookup CTA (one library each)
@@ -157,7 +157,6 @@ __device__ __forceinline__ double simplex_weight(double d2, int k, int lane) {
     return __ddiv_rn(u, sum);
 }
 
-constexpr double PAD_VALUE = 1e300;   // (q - PAD)^2 = +inf: out-of-range coordinates poison D
 constexpr float THR_EMPTY = 3.402823466e38f;  // FLT_MAX: an empty list admits every finite candidate
 // fp32 prefilter bound of a fp64 list distance D: the sweep accumulates D in fp32, whose
 // relative error is below (E+3) 2^-24 < 2^-18 for E <= 20 (fp32 inputs, no overflow), so any
@@ -189,8 +188,7 @@ __host__ __device__ constexpr size_t knn_warp_bytes(int L) {
     return (sizeof(KnnWarpSmem) + 15) / 16 * 16 + (size_t)knn_memb_words(L) * sizeof(unsigned);
 }
 constexpr size_t knn_smem_bytes(int L, int tau) {
-    return ((size_t)(knn_padl(tau) + L + KNN_PADR) * sizeof(double) + 15) / 16 * 16 +
-           (size_t)KNN_WARPS * knn_warp_bytes(L) + (size_t)(knn_padl(tau) + L + KNN_PADR) * sizeof(float);
+    return (size_t)KNN_WARPS * knn_warp_bytes(L) + (size_t)(knn_padl(tau) + L + KNN_PADR) * sizeof(float);
 }
 
 // Merge the lanes flagged in `bal` (candidates that passed list e's prefilter; distance `cand`
@@ -252,7 +250,7 @@ __device__ __forceinline__ double list_merge(KnnWarpSmem& W, int e, unsigned bal
 // same fp64 operation sequence as the oracle's C3 loop, so every D_E is bit-identical to the
 // oracle's) and, at every E in the selected set, a top-(E+1) list by (D_E, s).
 // Candidates outside P_E are never tested explicitly: the candidate series is padded on
-// both sides with PAD_VALUE, so a coordinate before the series start makes D = +inf from
+// both sides with 1e30, so a coordinate before the series start makes D = +inf from
 // that E on, and lanes past the candidate range / the excluded self start at D = +inf.
 // The sweep is branch-free per E: each E only compares against its prefilter bound and
 // records passing lanes; list insertions for all E run afterwards in one shared code path.
@@ -265,7 +263,6 @@ __device__ __forceinline__ double list_merge(KnnWarpSmem& W, int e, unsigned bal
 // result: the final list is the k smallest keys over all candidates either way.
 template <int MODE, bool TAU1, bool FULLMASK>
 __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, unsigned* memb, int mw,
-                                         const double* __restrict__ qa, const double* __restrict__ cb,
                                          const float* __restrict__ qaf, const float* __restrict__ cbf,
                                          int t_begin, int t_end, int ncand,
                                          unsigned mask, int Etop, int b, int lane) {
@@ -297,7 +294,7 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
             if (all && ok) {
                 D = 0.0;
                 for (int m = 0; m <= e; ++m) {
-                    const double diff = __dsub_rn(qa[t - m * tau], cb[c - m * tau]);
+                    const double diff = __dsub_rn((double)qaf[t - m * tau], (double)cbf[c - m * tau]);
                     D = __dadd_rn(D, __dmul_rn(diff, diff));
                 }
             }
@@ -335,12 +332,12 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
             // list merges for every E that had a passing lane in this chunk; the candidate
             // distances are recomputed (same operation sequence) up to the largest such E
             unsigned om = __reduce_or_sync(FULL, pass);
-            const double* cs = cb + s;
-            const double* qt = qa + t;
+            const float* cs = cbf + s;
+            const float* qt = qaf + t;
             double D = (s >= 0 && s < ncand && !(excl && s == t)) ? 0.0 : CUDART_INF;
             const int elast = 31 - __clz(om);
             for (int e = 0; e <= elast; ++e) {
-                const double diff = __dsub_rn(qt[-e * tau], cs[-e * tau]);
+                const double diff = __dsub_rn((double)qt[-e * tau], (double)cs[-e * tau]);
                 D = __dadd_rn(D, __dmul_rn(diff, diff));
                 if ((om >> e) & 1u) {
                     const unsigned bal = __ballot_sync(FULL, (pass >> e) & 1u);
@@ -459,27 +456,26 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
 template <int MODE, bool TAU1, bool FULLMASK>
 __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnParams P) {
     extern __shared__ __align__(16) unsigned char knn_smem[];
-    double* xs_pad = reinterpret_cast<double*>(knn_smem);
+
     const int b = blockIdx.y;
     const int row = P.slot_series ? P.slot_series[b] : b;
     const float* xg = P.X + (int64_t)row * P.ldx;
     const int padl = knn_padl(P.tau);
     const int nx = padl + P.L + KNN_PADR;
-    float* xf_pad = reinterpret_cast<float*>(knn_smem + ((size_t)nx * sizeof(double) + 15) / 16 * 16 +
-                                             (size_t)KNN_WARPS * knn_warp_bytes(P.L));
+    // the library series in shared memory, fp32 (the inputs are fp32: widening to fp64 where the
+    // exact distances are formed is lossless), padded with 1e30 ((q - 1e30)^2 = +inf in fp32)
+    float* xf_pad = reinterpret_cast<float*>(knn_smem + (size_t)KNN_WARPS * knn_warp_bytes(P.L));
     for (int i = threadIdx.x; i < nx; i += blockDim.x) {
         const int t = i - padl;
-        const float v = (t >= 0 && t < P.L) ? xg[t] : 1e30f;  // (q - 1e30)^2 = +inf in fp32
-        xs_pad[i] = (t >= 0 && t < P.L) ? (double)v : PAD_VALUE;
-        xf_pad[i] = v;
+        xf_pad[i] = (t >= 0 && t < P.L) ? xg[t] : 1e30f;
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned char* wbase = knn_smem + ((size_t)nx * sizeof(double) + 15) / 16 * 16 + (size_t)warp * knn_warp_bytes(P.L);
+    unsigned char* wbase = knn_smem + (size_t)warp * knn_warp_bytes(P.L);
     KnnWarpSmem& W = *reinterpret_cast<KnnWarpSmem*>(wbase);
     const int mw = knn_memb_words(P.L);
     unsigned* memb = mw ? reinterpret_cast<unsigned*>(wbase + (sizeof(KnnWarpSmem) + 15) / 16 * 16) : nullptr;
-    const double* xs = xs_pad + padl;
+
     unsigned mask = P.maskS;
     int Etop = P.Etop;
     if (P.slotE) {
@@ -487,28 +483,23 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnPa
         mask = 1u << e;
         Etop = e;
     }
-    const double* qa;
-    const double* cb;
     const float* xf = xf_pad + padl;
     const float* qaf;
     const float* cbf;
     int nq, ncand;
     if (MODE == MODE_SIMPLEX) {
         const int Llib = (P.L + 1) / 2;   // library = first ceil(L/2) samples
-        cb = xs;
-        qa = xs + Llib;
         cbf = xf;
         qaf = xf + Llib;
         nq = (P.L - Llib) - 1;            // target points t with t+1 inside the target half
         ncand = Llib - 1;                 // library points s with s+1 inside the library half
     } else {
-        qa = cb = xs;
         qaf = cbf = xf;
         nq = ncand = P.L - P.Tp;          // P_1 = [0, L-1-Tp]; per-E lower bound (E-1)tau
     }
     const int t0 = blockIdx.x * KNN_QPB + warp * KNN_QPW;
     const int t1 = min(nq, t0 + KNN_QPW);
-    if (t0 < t1) knn_warp<MODE, TAU1, FULLMASK>(P, W, memb, mw, qa, cb, qaf, cbf, t0, t1, ncand, mask, Etop, b, lane);
+    if (t0 < t1) knn_warp<MODE, TAU1, FULLMASK>(P, W, memb, mw, qaf, cbf, t0, t1, ncand, mask, Etop, b, lane);
 }
 
 // Weights of the phase-2 tables (S8, C5), one thread per table row: the kNN kernel
