@@ -173,7 +173,7 @@ def run_reference(args):
     L, N = data.shape
     from oracle import oracle as O
     n_series = min(N, 64)
-    n_lib = min(N, args.cpu_sample or 16)
+    n_lib = min(N, args.cpu_sample or 48)
     # E for the phase-2 sample: the oracle's own phase 1 on the whole set would be too slow at
     # c3; use E from the oracle on the sampled series for those, and the sample's mode for the rest
     # phase 2 needs every target's E; the oracle's phase 1 over all N series would take far
@@ -405,8 +405,8 @@ def main():
     # ---- CPU baseline: the oracle on a bounded sample, rank 0 at N=1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_lib = args.cpu_sample or min(N, 32)
-        v, secs, cores, desc = oracle_sample(host, E_host, args.mode, tau, Tp, n_lib, min(N, 64))
+        n_lib = args.cpu_sample or min(N, 128)
+        v, secs, cores, desc = oracle_sample(host, E_host, args.mode, tau, Tp, n_lib, min(N, 256))
         cpu = {"value": v, "unit": "pairs/s", "cores": cores, "kind": "oracle", "sample": desc}
 
     if rank == 0:
