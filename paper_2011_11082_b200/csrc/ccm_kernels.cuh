@@ -22,7 +22,10 @@ constexpr int ECAP = 20;            // largest E (k = E + 1 <= 21 <= 32 lanes)
 constexpr int TILE_J = 32;          // targets per lookup tile (one per lane)
 constexpr int KNN_WARPS = 4;        // warps per knn CTA
 constexpr int KNN_MIN_CTAS = 5;     // resident CTAs per SM the register budget must allow
-constexpr int KNN_QPW = 64;         // consecutive queries per warp
+#ifndef CCM_KNN_QPW
+#define CCM_KNN_QPW 24
+#endif
+constexpr int KNN_QPW = CCM_KNN_QPW;  // consecutive queries per warp
 constexpr int KNN_QPB = KNN_WARPS * KNN_QPW;
 constexpr int LOOKUP_WARPS = 16;    // warps per lookup CTA (one library each)
 constexpr unsigned FULL = 0xffffffffu;
@@ -170,7 +173,10 @@ constexpr int KNN_PADR = 32;
 // loff(e) + j, k = e + 2 entries) and the per-E prefilter bounds.
 __host__ __device__ constexpr int loff(int e) { return e * (e + 3) / 2; }
 constexpr int LIST_ENTRIES = loff(ECAP);  // 230
-constexpr int KNN_UMAX = 96;  // candidates of the union pre-pass (3 pseudo-chunks)
+#ifndef CCM_KNN_UMAX
+#define CCM_KNN_UMAX 96
+#endif
+constexpr int KNN_UMAX = CCM_KNN_UMAX;  // candidates of the union pre-pass (up to 3 pseudo-chunks)
 struct KnnWarpSmem {
     double D[LIST_ENTRIES];
     int S[LIST_ENTRIES];

@@ -49,7 +49,7 @@ def load(path: Optional[str] = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or _build.LIB
+    path = path or os.environ.get("LIBCCM_PATH") or _build.LIB
     if not os.path.exists(path):
         raise ImportError(f"libccm.so not found at {path}; run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = C.CDLL(path)
