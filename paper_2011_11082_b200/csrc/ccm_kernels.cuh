@@ -661,8 +661,18 @@ struct LookupParams {
 
 // ---- per-warp table staging: TMA bulk copies (cp.async.bulk) into a 2-stage shared-memory
 // ring, completion tracked by an mbarrier per stage (expect_tx / complete_tx).
-constexpr int LK_CHUNK = 1024;  // bytes per stage
-constexpr int LK_STAGES = 2;
+#ifndef CCM_LK_CHUNK
+#define CCM_LK_CHUNK 1024
+#endif
+#ifndef CCM_LK_STAGES
+#define CCM_LK_STAGES 2
+#endif
+#ifndef CCM_LK_UNROLL
+#define CCM_LK_UNROLL 2
+#endif
+constexpr int LK_CHUNK = CCM_LK_CHUNK;    // bytes per stage
+constexpr int LK_STAGES = CCM_LK_STAGES;
+constexpr int LK_UNROLL = CCM_LK_UNROLL;  // rows in flight per warp
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -723,8 +733,9 @@ __device__ __forceinline__ void lookup_one(const LookupParams& P, const float* _
     };
     if (lane == 0) {
         fence_proxy_async();  // earlier generic reads of the ring before the async-proxy writes
-        issue(0, R.it % LK_STAGES);
-        if (nch > 1) issue(1, (R.it + 1) % LK_STAGES);
+#pragma unroll
+        for (int i = 0; i < LK_STAGES; ++i)
+            if (i < nch) issue(i, (R.it + i) % LK_STAGES);
     }
     double Sp = 0.0, Spp = 0.0, Spo = 0.0;
     const float* Yo = Y + (int64_t)(t0 + P.Tp) * ys + lane;
@@ -736,7 +747,7 @@ __device__ __forceinline__ void lookup_one(const LookupParams& P, const float* _
         const uint4* rowp = R.buf + slot * (LK_CHUNK / 16);
         const int r0 = ci * ROWS, r1 = min(n, r0 + ROWS);
         float sp = 0.f, spp = 0.f, spo = 0.f;
-#pragma unroll 2
+#pragma unroll LK_UNROLL
         for (int r = r0; r < r1; ++r) {
             const uint4* row = rowp + (r - r0) * (kp / 2);
             float p = 0.f;
@@ -758,9 +769,9 @@ __device__ __forceinline__ void lookup_one(const LookupParams& P, const float* _
         Spo += (double)spo;
         __syncwarp();  // every lane is done reading this stage
         ++R.it;
-        if (lane == 0 && ci + 2 < nch) {
+        if (lane == 0 && ci + LK_STAGES < nch) {
             fence_proxy_async();
-            issue(ci + 2, slot);
+            issue(ci + LK_STAGES, slot);
         }
     }
     if (col >= 0) {
