@@ -112,6 +112,19 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t *E, int32_t tau, int3
                              int32_t lib_end, float *rho, void *workspace, size_t ws_bytes,
                              void *stream);
 
+/* Time-delay cross mapping ("The adjacency in the network is determined
+ * by time delay cross mapping"): the phase-2 map at every lag l in [lag_min, lag_max] (l may be
+ * negative) from ONE set of kNN tables per library block. Tables are built on the points
+ *   P_E = { t : (E-1)tau + m_lo <= t <= L-1-m_hi },  m_lo = max(0, -lag_min), m_hi = max(0, lag_max),
+ * (candidates P_E minus {t}), so that y[t+l] and y[s+l] exist for every lag; then
+ *   rho[((i - lib_begin) * nlag + (l - lag_min)) * N + j] = Pearson_t( sum_k w_k y_j[s_k + l], y_j[t + l] ),
+ * nlag = lag_max - lag_min + 1. With lag_min = lag_max = Tp >= 0 this equals edm_ccm_all_pairs(Tp).
+ * Same conventions and errors as edm_ccm_all_pairs; workspace >= edm_ccm_lagged_workspace_bytes. */
+edm_status edm_ccm_lagged(edm_dataset ds, const int32_t *E, int32_t tau, int32_t lag_min, int32_t lag_max,
+                          edm_e_mode mode, int32_t exclude_self, int32_t lib_begin, int32_t lib_end, float *rho,
+                          void *workspace, size_t ws_bytes, void *stream);
+size_t edm_ccm_lagged_workspace_bytes(int32_t N, int32_t L, int32_t tau, int32_t lag_min, int32_t lag_max);
+
 /* Scratch size in bytes for which = 0 (edm_simplex_optimal_E over N series) or
  * which = 1 (edm_ccm_all_pairs over an N-series dataset; E_max = largest E in E[]).
  * Returns 0 for invalid arguments. */

@@ -240,6 +240,7 @@ int oracle_simplex(const double *x, int L, int E_max, int tau, double *rhoE, int
 typedef struct {
     const float *data; int N, L; long ld;
     int E_max, tau, Tp, mode, excl, naive;
+    int lag_min, lag_max;
     const int *E;
     int begin, end;
     int *optE; double *rhoE; double *rho;
@@ -371,4 +372,96 @@ int oracle_ccm_rows(const float *data, int N, int L, long ld, const int *E, int 
     J.mode = mode; J.excl = exclude_self; J.naive = naive;
     J.begin = lib_begin; J.end = lib_end; J.rho = rho;
     return run_pool(&J, ccm_worker, nthreads);
+}
+
+/* ---------------------------------------------------------------- time-delay cross mapping */
+/* SURVEY 8(f) f1 / PAPER.md P:214 ("The adjacency in the network is determined by time delay
+ * cross mapping"): the cross-map skill of target j from library i's manifold at every lag l in
+ * [lag_min, lag_max] (l may be negative): p_l(t) = sum_k w_k y[s_k + l], o_l(t) = y[t + l],
+ * rho_l = Pearson(p_l, o_l) over the rows t. One table per (library, E) serves every lag, so
+ * rows and candidates are the points whose shifted values exist for every lag:
+ *   P_E = { t : (E-1)tau + m_lo <= t <= L-1-m_hi },  m_lo = max(0, -lag_min), m_hi = max(0, lag_max),
+ * candidates P_E \ {t} (exclude_self). With lag_min = lag_max = Tp >= 0 this is exactly the
+ * phase-2 map of oracle_ccm_rows at horizon Tp. Output rho[((i-lib_begin)*nlag + l-lag_min)*N + j]. */
+static int lagged_row(const job_t *J, int i, double *x, double *y, double *out) {
+    const int L = J->L, tau = J->tau, N = J->N;
+    const int nlag = J->lag_max - J->lag_min + 1;
+    const int m_lo = J->lag_min < 0 ? -J->lag_min : 0, m_hi = J->lag_max > 0 ? J->lag_max : 0;
+    int Ecap = J->E[i];
+    for (int j = 0; j < N; ++j) if (J->E[j] > Ecap) Ecap = J->E[j];
+    int **tidx = (int **)calloc(Ecap + 1, sizeof(int *));
+    double **tw = (double **)calloc(Ecap + 1, sizeof(double *));
+    double *d2 = (double *)malloc(sizeof(double) * (size_t)L * (Ecap + 1));
+    double *p = (double *)malloc(sizeof(double) * L);
+    double *o = (double *)malloc(sizeof(double) * L);
+    int rc = OR_OK;
+    if (!tidx || !tw || !d2 || !p || !o) { rc = OR_ENOMEM; goto done; }
+    load_series(J->data, J->ld, L, i, x);
+    for (int j = 0; j < N && rc == OR_OK; ++j) {
+        const int E = (J->mode == 0) ? J->E[j] : J->E[i];
+        const int k = E + 1;
+        const int lo = (E - 1) * tau + m_lo, hi = L - 1 - m_hi, n = hi - lo + 1;
+        if (!tidx[E]) {
+            tidx[E] = (int *)malloc(sizeof(int) * (size_t)n * k);
+            tw[E] = (double *)malloc(sizeof(double) * (size_t)n * k);
+            if (!tidx[E] || !tw[E]) { rc = OR_ENOMEM; break; }
+            int r = oracle_knn(x, lo, hi, x, lo, hi, E, tau, J->excl, tidx[E], d2);
+            if (r < 0) { rc = r; break; }
+            for (int q = 0; q < n; ++q) oracle_weights(d2 + (size_t)q * k, k, tw[E] + (size_t)q * k);
+        }
+        load_series(J->data, J->ld, L, j, y);
+        for (int l = J->lag_min; l <= J->lag_max; ++l) {
+            for (int r = 0; r < n; ++r) {
+                double acc = 0.0;
+                for (int m = 0; m < k; ++m)
+                    acc = acc + tw[E][(size_t)r * k + m] * y[tidx[E][(size_t)r * k + m] + l];
+                p[r] = acc;
+                o[r] = y[lo + r + l];
+            }
+            out[(size_t)(l - J->lag_min) * N + j] = oracle_pearson(p, o, n);
+        }
+    }
+done:
+    if (tidx) for (int E = 0; E <= Ecap; ++E) free(tidx[E]);
+    if (tw) for (int E = 0; E <= Ecap; ++E) free(tw[E]);
+    free(tidx); free(tw); free(d2); free(p); free(o);
+    (void)nlag;
+    return rc;
+}
+
+static void *lagged_worker(void *arg) {
+    job_t *J = (job_t *)arg;
+    double *x = (double *)malloc(sizeof(double) * J->L);
+    double *y = (double *)malloc(sizeof(double) * J->L);
+    const int nlag = J->lag_max - J->lag_min + 1;
+    if (!x || !y) { J->err = OR_ENOMEM; free(x); free(y); return NULL; }
+    for (;;) {
+        int r = __sync_fetch_and_add(&J->next, 1);
+        if (r >= J->end - J->begin || J->err) break;
+        int rc = lagged_row(J, J->begin + r, x, y, J->rho + (size_t)r * nlag * J->N);
+        if (rc != OR_OK) J->err = rc;
+    }
+    free(x); free(y);
+    return NULL;
+}
+
+int oracle_ccm_lagged_rows(const float *data, int N, int L, long ld, const int *E, int tau, int lag_min,
+                           int lag_max, int mode, int exclude_self, int lib_begin, int lib_end, double *rho,
+                           int nthreads) {
+    if (!data || !E || !rho || N < 1 || L < 2 || tau < 1 || lag_min > lag_max || lib_begin < 0 ||
+        lib_end > N || lib_begin > lib_end || (mode != 0 && mode != 1))
+        return OR_EINVAL;
+    const int m_lo = lag_min < 0 ? -lag_min : 0, m_hi = lag_max > 0 ? lag_max : 0;
+    for (int j = 0; j < N; ++j) {
+        if (E[j] < 1) return OR_EINVAL;
+        int n = L - (E[j] - 1) * tau - m_lo - m_hi;
+        if (n - (exclude_self ? 1 : 0) < E[j] + 1) return OR_ETOOSHORT;
+    }
+    job_t J;
+    memset(&J, 0, sizeof(J));
+    J.data = data; J.N = N; J.L = L; J.ld = ld; J.E = E; J.tau = tau;
+    J.lag_min = lag_min; J.lag_max = lag_max;
+    J.mode = mode; J.excl = exclude_self;
+    J.begin = lib_begin; J.end = lib_end; J.rho = rho;
+    return run_pool(&J, lagged_worker, nthreads);
 }

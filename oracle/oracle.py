@@ -59,6 +59,8 @@ def lib():
         _lib.oracle_simplex_all.argtypes = [fp, i, i, C.c_long, i, i, i, i, ip, dp, i]
         _lib.oracle_ccm_rows.restype = i
         _lib.oracle_ccm_rows.argtypes = [fp, i, i, C.c_long, ip, i, i, i, i, i, i, i, dp, i]
+        _lib.oracle_ccm_lagged_rows.restype = i
+        _lib.oracle_ccm_lagged_rows.argtypes = [fp, i, i, C.c_long, ip, i, i, i, i, i, i, i, dp, i]
     return _lib
 
 
@@ -188,4 +190,20 @@ def ccm_rows(data, E, tau=1, Tp=1, mode=MODE_TARGET, exclude_self=True, lib_begi
     _check(lib().oracle_ccm_rows(pd, N, L, N, pe, tau, Tp, mode, int(exclude_self), lib_begin, lib_end, int(naive),
                                  rho.ctypes.data_as(C.POINTER(C.c_double)), nthreads or nthreads_default()),
            "ccm_rows")
+    return rho
+
+
+def ccm_lagged_rows(data, E, tau=1, lag_min=-2, lag_max=2, mode=MODE_TARGET, exclude_self=True, lib_begin=0,
+                    lib_end=None, nthreads=None):
+    """Time-delay cross mapping: rho [rows, nlags, N] fp64 for lags
+    lag_min..lag_max from one table per (library, E) over the points valid for every lag."""
+    data, pd = _f(data)
+    L, N = data.shape
+    E, pe = _i(E)
+    lib_end = N if lib_end is None else lib_end
+    nlag = lag_max - lag_min + 1
+    rho = np.zeros((lib_end - lib_begin, nlag, N), np.float64)
+    _check(lib().oracle_ccm_lagged_rows(pd, N, L, N, pe, tau, lag_min, lag_max, mode, int(exclude_self), lib_begin,
+                                        lib_end, rho.ctypes.data_as(C.POINTER(C.c_double)),
+                                        nthreads or nthreads_default()), "ccm_lagged_rows")
     return rho

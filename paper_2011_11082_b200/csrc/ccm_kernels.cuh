@@ -53,57 +53,61 @@ __global__ void transpose_kernel(const float* __restrict__ in, int64_t ld, int L
 }
 
 // ------------------------------------------------------------------ S5 target preparation
-// mean[j] = fp64 mean of series j; lastdiff[j] = largest t with y[t] != y[L-1] (-1 if constant).
-__global__ void colprep_kernel(const float* __restrict__ y, int64_t ld, int N, int L,
-                               double* __restrict__ mean, int* __restrict__ lastdiff) {
+// mean[j] = fp64 mean of series j.
+__global__ void colprep_kernel(const float* __restrict__ y, int64_t ld, int N, int L, double* __restrict__ mean) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= N) return;
     double s = 0.0;
     for (int t = 0; t < L; ++t) s += (double)y[(int64_t)t * ld + j];
     mean[j] = s / L;
-    const float last = y[(int64_t)(L - 1) * ld + j];
-    int ld_ = -1;
-    for (int t = L - 2; t >= 0; --t)
-        if (y[(int64_t)t * ld + j] != last) { ld_ = t; break; }
-    lastdiff[j] = ld_;
 }
 
 // Yp[t][p] = y[t][colmap[p]] - mean[colmap[p]] (0 for padding columns colmap[p] < 0).
-// Also lastdiff_p[p] = lastdiff[colmap[p]] (-1 for padding).
 __global__ void permute_kernel(const float* __restrict__ y, int64_t ld, int L, int Np,
                                const int* __restrict__ colmap, const double* __restrict__ mean,
-                               const int* __restrict__ lastdiff, float* __restrict__ Yp,
-                               int* __restrict__ lastdiff_p) {
+                               float* __restrict__ Yp) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= Np) return;
     const int c = colmap[p];
     const double mu = c >= 0 ? mean[c] : 0.0;
-    if (blockIdx.y == 0) lastdiff_p[p] = c >= 0 ? lastdiff[c] : -1;
     for (int t = blockIdx.y; t < L; t += gridDim.y)
         Yp[(int64_t)t * Np + p] = c >= 0 ? (float)((double)y[(int64_t)t * ld + c] - mu) : 0.f;
 }
 
-// Observed-window sums for every E: the observation of row t is y[t+Tp], t in
-// P_E = [(E-1)tau, L-1-Tp], i.e. the suffix y[(E-1)tau+Tp .. L-1].
-// stats[(E-1)*Np + p] = (sum y, sum y^2) over that suffix of the centred fp32 column.
-__global__ void stats_kernel(const float* __restrict__ Yp, int L, int Np, int tau, int Tp, int Emax,
-                             double2* __restrict__ stats) {
+// Observed-window statistics for every E: the observation of table row r
+// at E is y[(E-1)tau + d + r], r < n_E, i.e. the window [(E-1)tau + d, obs_end] (obs_end is
+// the same for every E). stats[(E-1)*Np + p] = (sum y, sum y^2) of the centred fp32 column
+// over it (fp64), cflag[(E-1)*Np + p] = 1 if every raw value in it is equal (NaN skill).
+// Single-horizon CCM: d = Tp, obs_end = L-1; time-delay cross map: d = m_lo + lag.
+__global__ void stats_kernel(const float* __restrict__ Yp, const float* __restrict__ y, int64_t ld,
+                             const int* __restrict__ colmap, int Np, int tau, int d, int obs_end, int Emax,
+                             double2* __restrict__ stats, int* __restrict__ cflag) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= Np) return;
+    const int c = colmap[p];
     double s1 = 0.0, s2 = 0.0;
-    int e = Emax;  // next E to record, descending: start index (e-1)tau+Tp increases with e
-    for (; e >= 1 && (e - 1) * tau + Tp > L - 1; --e)  // empty window: infeasible E
+    bool same = true;
+    const float last = c >= 0 ? y[(int64_t)obs_end * ld + c] : 0.f;
+    int e = Emax;  // next E to record, descending: start index (e-1)tau+d increases with e
+    for (; e >= 1 && (e - 1) * tau + d > obs_end; --e) {  // empty window: infeasible E
         stats[(int64_t)(e - 1) * Np + p] = make_double2(0.0, 0.0);
-    for (int t = L - 1; t >= 0 && e >= 1; --t) {
+        cflag[(int64_t)(e - 1) * Np + p] = 1;
+    }
+    for (int t = obs_end; t >= 0 && e >= 1; --t) {
         const double v = (double)Yp[(int64_t)t * Np + p];
         s1 += v;
         s2 += v * v;
-        while (e >= 1 && t == (e - 1) * tau + Tp) {
+        if (c >= 0 && y[(int64_t)t * ld + c] != last) same = false;
+        while (e >= 1 && t == (e - 1) * tau + d) {
             stats[(int64_t)(e - 1) * Np + p] = make_double2(s1, s2);
+            cflag[(int64_t)(e - 1) * Np + p] = same ? 1 : 0;
             --e;
         }
     }
-    for (; e >= 1; --e) stats[(int64_t)(e - 1) * Np + p] = make_double2(0.0, 0.0);  // infeasible E
+    for (; e >= 1; --e) {
+        stats[(int64_t)(e - 1) * Np + p] = make_double2(0.0, 0.0);
+        cflag[(int64_t)(e - 1) * Np + p] = 1;
+    }
 }
 
 // ------------------------------------------------------------------ kNN (S1/S6, S7, S8)
@@ -111,7 +115,8 @@ struct KnnParams {
     const float* X;         // series-major rows (MODE_CCM/SIMPLEX) or the single series (EMBED)
     int64_t ldx;            // row stride of X
     const int* slot_series; // X row of block slot b (NULL: b)
-    int L, tau, Tp, excl;
+    int L, tau, Tp, excl;   // Tp: table horizon (rows/candidates t <= L-1-Tp)
+    int store_shift;        // MODE_CCM: stored label = s + store_shift
     unsigned maskS;         // bit E set <=> a list is kept at E (target mode / simplex / embed)
     int Etop;               // largest E needed
     const int* slotE;       // library mode: E of slot b (overrides maskS/Etop); NULL otherwise
@@ -433,7 +438,7 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
                 // {s + Tp, fp32 distance}; weights_kernel turns the distance into the weight
                 const int kp = kpad(k);
                 if (lane < kp) {
-                    uint2 ent = lane < k ? make_uint2((unsigned)(sl + P.Tp), __float_as_uint((float)sqrt(d2)))
+                    uint2 ent = lane < k ? make_uint2((unsigned)(sl + P.store_shift), __float_as_uint((float)sqrt(d2)))
                                          : make_uint2(0u, 0u);
                     P.tables[(int64_t)b * P.T_lib + P.offE[e + 1] + (int64_t)row * kp + lane] = ent;
                 }
@@ -653,10 +658,14 @@ struct LookupParams {
     const uint2* tables;
     int64_t T_lib;
     int64_t offE[ECAP + 2];
-    const double2* stats;   // [ECAP][Np]
-    const int* lastdiff;    // [Np] (per permuted column)
-    int L, tau, Tp, B, N;
-    float* rho;
+    const double2* stats;   // [ECAP][Np] observed-window sums
+    const int* cflag;       // [ECAP][Np] observed window constant
+    int Lt;                 // rows of the target tile (series length)
+    int Lk, hrz;            // table rows at E: n_E = Lk - (E-1) tau - hrz
+    int gshift, oshift;     // gather y[label + gshift]; observe y[(E-1)tau + oshift + r]
+    int tau, B, N;
+    float* rho;             // rho[slotRow * rstride + roff + col]
+    int64_t rstride, roff;
 };
 
 // ---- per-warp table staging: TMA bulk copies (cp.async.bulk) into a 2-stage shared-memory
@@ -725,7 +734,7 @@ __device__ __forceinline__ void lookup_one(const LookupParams& P, const float* _
     constexpr int CB = ROWS * kp * 8;               // bytes of a full chunk (multiple of 16)
     const char* tab = reinterpret_cast<const char*>(P.tables + (int64_t)b * P.T_lib + P.offE[E]);
     const int t0 = (E - 1) * P.tau;
-    const int n = P.L - t0 - P.Tp;
+    const int n = P.Lk - t0 - P.hrz;
     const int nch = (n + ROWS - 1) / ROWS;
     auto issue = [&](int ci, uint32_t slot) {
         const int rows = min(ROWS, n - ci * ROWS);
@@ -738,8 +747,14 @@ __device__ __forceinline__ void lookup_one(const LookupParams& P, const float* _
             if (i < nch) issue(i, (R.it + i) % LK_STAGES);
     }
     double Sp = 0.0, Spp = 0.0, Spo = 0.0;
-    const float* Yo = Y + (int64_t)(t0 + P.Tp) * ys + lane;
-    const float* Yl = Y + lane;
+    const float* Yo = Y + (int64_t)(t0 + P.oshift) * ys + lane;
+    // the lag shift is folded into the lane's base offset (opaque to the compiler, so that it
+    // is not re-applied to every gathered index)
+    const char* Yb = reinterpret_cast<const char*>(Y);
+    const uint32_t rowb = (uint32_t)(ys * sizeof(float));
+    uint32_t lbase = (uint32_t)((P.gshift * ys + lane) * sizeof(float));
+    asm("" : "+r"(lbase));
+    auto Yl = [&](uint32_t idx) { return *reinterpret_cast<const float*>(Yb + (idx * rowb + lbase)); };
     float c = 0.f;  // shift: the first prediction (no cancellation for near-constant predictions)
     for (int ci = 0; ci < nch; ++ci) {
         const uint32_t slot = R.it % LK_STAGES;
@@ -754,8 +769,8 @@ __device__ __forceinline__ void lookup_one(const LookupParams& P, const float* _
 #pragma unroll
             for (int j2 = 0; j2 < kp / 2; ++j2) {
                 const uint4 e2 = row[j2];
-                p = fmaf(__uint_as_float(e2.y), Yl[(int64_t)e2.x * ys], p);
-                if (2 * j2 + 1 < k) p = fmaf(__uint_as_float(e2.w), Yl[(int64_t)e2.z * ys], p);
+                p = fmaf(__uint_as_float(e2.y), Yl(e2.x), p);
+                if (2 * j2 + 1 < k) p = fmaf(__uint_as_float(e2.w), Yl(e2.z), p);
             }
             if (r == 0) c = p;
             p -= c;
@@ -777,14 +792,14 @@ __device__ __forceinline__ void lookup_one(const LookupParams& P, const float* _
     if (col >= 0) {
         const int pcol = tile * TILE_J + lane;
         const double2 st = P.stats[(int64_t)(E - 1) * P.Np + pcol];
-        const bool o_const = P.lastdiff[pcol] < t0 + P.Tp;  // every observed value equal
+        const bool o_const = P.cflag[(int64_t)(E - 1) * P.Np + pcol] != 0;  // every observed value equal
         const double nn = (double)n;
         const double cov = Spo - Sp * st.x / nn;
         const double vp = Spp - Sp * Sp / nn;
         const double vo = st.y - st.x * st.x / nn;
         float r = CUDART_NAN_F;
         if (!o_const && vp > 0.0 && vo > 0.0) r = (float)(cov / sqrt(vp * vo));
-        P.rho[(int64_t)P.slotRow[b] * P.N + col] = r;
+        P.rho[(int64_t)P.slotRow[b] * P.rstride + P.roff + col] = r;
     }
 }
 
@@ -816,7 +831,7 @@ __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupPara
     const int Et = P.tileE ? P.tileE[tile] : 0;
     if (P.tileE && Et <= 0) return;
     float* ytile = reinterpret_cast<float*>(lk_smem);
-    const size_t tile_bytes = SMEM ? (size_t)P.L * TILE_J * sizeof(float) : 0;
+    const size_t tile_bytes = SMEM ? (size_t)P.Lt * TILE_J * sizeof(float) : 0;
     uint4* ring = reinterpret_cast<uint4*>(lk_smem + tile_bytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(lk_smem + tile_bytes + (size_t)LOOKUP_WARPS * LK_STAGES * LK_CHUNK);
     WarpRing R{ring + (size_t)warp * LK_STAGES * (LK_CHUNK / 16), bars + warp * LK_STAGES, 0u};
@@ -828,7 +843,7 @@ __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupPara
     int64_t ys;
     if (SMEM) {
         const float* src = P.Yp + (int64_t)tile * TILE_J;
-        for (int i = threadIdx.x; i < P.L * (TILE_J / 4); i += blockDim.x) {
+        for (int i = threadIdx.x; i < P.Lt * (TILE_J / 4); i += blockDim.x) {
             const int t = i / (TILE_J / 4), c = (i % (TILE_J / 4)) * 4;
             *reinterpret_cast<float4*>(ytile + t * TILE_J + c) =
                 __ldg(reinterpret_cast<const float4*>(src + (int64_t)t * P.Np + c));

@@ -143,11 +143,10 @@ struct CcmWs {
     float* Xs;          // [N][L] library series, series-major
     float* Yp;          // [L][Npm] centred permuted targets
     int* colmap;        // [Npm]
-    int* lastdiff_p;    // [Npm]
     int* tileE;         // [Npm / 32]
     double* mean;       // [N]
-    int* lastdiff;      // [N]
-    double2* stats;     // [ECAP][Npm]
+    double2* stats;     // [nlag][ECAP][Npm] observed-window sums
+    int* cflag;         // [nlag][ECAP][Npm] observed window constant
     int* slot_series;   // [N]
     int* slot_row;      // [N]
     int* slotE;         // [N]
@@ -156,10 +155,11 @@ struct CcmWs {
     size_t bytes;
 };
 
-CcmWs ccm_ws(void* base, int N, int L, int tau, int Tp) {
+// Lk / hrz: the table geometry (rows n_E = Lk - (E-1)tau - hrz); nlag observation windows.
+CcmWs ccm_ws(void* base, int N, int L, int Lk, int tau, int hrz, int nlag) {
     CcmWs w{};
     int64_t offE[ECAP + 2];
-    table_layout(L, tau, Tp, offE, &w.T_lib);
+    table_layout(Lk, tau, hrz, offE, &w.T_lib);
     w.Npm = np_max(N);
     size_t off = 0;
     char* b = (char*)base;
@@ -167,11 +167,10 @@ CcmWs ccm_ws(void* base, int N, int L, int tau, int Tp) {
     w.Xs = (float*)take((size_t)N * L * sizeof(float));
     w.Yp = (float*)take((size_t)L * w.Npm * sizeof(float));
     w.colmap = (int*)take((size_t)w.Npm * sizeof(int));
-    w.lastdiff_p = (int*)take((size_t)w.Npm * sizeof(int));
     w.tileE = (int*)take((size_t)(w.Npm / TILE_J) * sizeof(int));
     w.mean = (double*)take((size_t)N * sizeof(double));
-    w.lastdiff = (int*)take((size_t)N * sizeof(int));
-    w.stats = (double2*)take((size_t)ECAP * w.Npm * sizeof(double2));
+    w.stats = (double2*)take((size_t)nlag * ECAP * w.Npm * sizeof(double2));
+    w.cflag = (int*)take((size_t)nlag * ECAP * w.Npm * sizeof(int));
     w.slot_series = (int*)take((size_t)N * sizeof(int));
     w.slot_row = (int*)take((size_t)N * sizeof(int));
     w.slotE = (int*)take((size_t)N * sizeof(int));
@@ -239,7 +238,7 @@ const char* edm_version(void) { return "libccm 0.1 sm_100a (fp64 exact kNN, fp32
 size_t edm_workspace_bytes(int32_t which, int32_t N, int32_t L, int32_t E_max, int32_t tau, int32_t Tp) {
     if (N < 1 || L < 2 || E_max < 1 || E_max > ECAP || tau < 1 || Tp < 0) return 0;
     if (which == 0) return simplex_ws(nullptr, N, L, E_max).bytes;
-    if (which == 1) return ccm_ws(nullptr, N, L, tau, Tp).bytes;
+    if (which == 1) return ccm_ws(nullptr, N, L, L, tau, Tp, 1).bytes;
     return 0;
 }
 
@@ -321,19 +320,22 @@ edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int
     return EDM_OK;
 }
 
-edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int32_t Tp, edm_e_mode mode,
-                             int32_t exclude_self, int32_t lib_begin, int32_t lib_end, float* rho, void* workspace,
-                             size_t ws_bytes, void* stream) {
-    if (!ds.data || !E || !rho || !workspace) return fail(EDM_EINVAL, "null pointer");
-    if (ds.N < 1 || ds.L < 2 || ds.ld < ds.N || tau < 1 || Tp < 0 || (mode != EDM_E_TARGET && mode != EDM_E_LIBRARY))
-        return fail(EDM_EINVAL, "bad arguments N=%d L=%d ld=%lld tau=%d Tp=%d mode=%d", ds.N, ds.L, (long long)ds.ld, tau, Tp, (int)mode);
-    if (lib_begin < 0 || lib_end > ds.N || lib_begin > lib_end) return fail(EDM_EINVAL, "bad library range [%d,%d)", lib_begin, lib_end);
-    const size_t need = edm_workspace_bytes(1, ds.N, ds.L, ECAP, tau, Tp);
+}  // extern "C"
+
+namespace {
+
+// Phase 2 core, shared by edm_ccm_all_pairs (one horizon Tp: m_lo = 0, m_hi = Tp, lags [Tp,Tp])
+// and edm_ccm_lagged (lags [lag_min, lag_max]). Tables are built once per library block on the
+// points t in [(E-1)tau + m_lo, L-1-m_hi] (the kNN runs on the series shifted by m_lo, with
+// horizon m_hi) and store the shifted label s - m_lo; each lag l is one lookup pass that reads
+// y[label + m_lo + l] and observes y[t + l]. rho[row * nlag*N + (l - lag_min) * N + j].
+edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int m_hi, int lag_min, int lag_max,
+                    edm_e_mode mode, int32_t exclude_self, int32_t lib_begin, int32_t lib_end, float* rho,
+                    void* workspace, size_t ws_bytes, size_t need, cudaStream_t cs) {
     if (need == 0 || ws_bytes < need) return fail(EDM_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
     edm_status st = check_device();
     if (st != EDM_OK) return st;
-    cudaStream_t cs = (cudaStream_t)stream;
-    const int N = ds.N, L = ds.L;
+    const int N = ds.N, L = ds.L, Lk = L - m_lo, nlag = lag_max - lag_min + 1;
 
     // ---- validate E[] and plan on the host (one small D2H copy)
     std::vector<int32_t> hE(N);
@@ -344,15 +346,16 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int3
     for (int j = 0; j < N; ++j) {
         const int e = hE[j];
         if (e < 1 || e > ECAP) return fail(EDM_EINVAL, "E[%d]=%d outside [1,%d]", j, e, ECAP);
-        if (n_rows(L, e, tau, Tp) - (exclude_self ? 1 : 0) < e + 1)
-            return fail(EDM_ETOOSHORT, "E[%d]=%d leaves fewer than E+1 candidates at L=%d tau=%d Tp=%d", j, e, L, tau, Tp);
+        if (n_rows(Lk, e, tau, m_hi) - (exclude_self ? 1 : 0) < e + 1)
+            return fail(EDM_ETOOSHORT, "E[%d]=%d leaves fewer than E+1 candidates at L=%d tau=%d (margins %d, %d)", j, e,
+                        L, tau, m_lo, m_hi);
         maskS |= 1u << e;
         Etop = std::max(Etop, e);
     }
     if (lib_begin == lib_end) return EDM_OK;
-    CcmWs W = ccm_ws(workspace, N, L, tau, Tp);
+    CcmWs W = ccm_ws(workspace, N, L, Lk, tau, m_hi, nlag);
     int64_t offE[ECAP + 2], T_lib;
-    table_layout(L, tau, Tp, offE, &T_lib);
+    table_layout(Lk, tau, m_hi, offE, &T_lib);
 
     // target ordering (S5): target mode -> stable counting sort by (E_j, j), every E segment
     // padded to a multiple of 32 so that a 32-target tile has one E; library mode -> identity.
@@ -389,21 +392,26 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int3
     CUDA_TRY(cudaMemcpyAsync(W.slot_row, srow.data(), sizeof(int) * nlib, cudaMemcpyHostToDevice, cs));
     CUDA_TRY(cudaMemcpyAsync(W.slotE, sE.data(), sizeof(int) * nlib, cudaMemcpyHostToDevice, cs));
 
-    // ---- ingest and target preparation (S0, S5)
+    // ---- ingest and target preparation (S0, S5); one set of window statistics per lag
     {
         dim3 tb(32, 8), tg((nlib + 31) / 32, (L + 31) / 32);
         PROF_LAUNCH(EDM_PROF_PREP, cs, transpose_kernel<<<tg, tb, 0, cs>>>(ds.data, ds.ld, L, lib_begin, nlib, W.Xs));
         LAUNCH_CHECK("transpose_kernel");
-        PROF_LAUNCH(EDM_PROF_PREP, cs, colprep_kernel<<<(N + 127) / 128, 128, 0, cs>>>(ds.data, ds.ld, N, L, W.mean, W.lastdiff));
+        PROF_LAUNCH(EDM_PROF_PREP, cs, colprep_kernel<<<(N + 127) / 128, 128, 0, cs>>>(ds.data, ds.ld, N, L, W.mean));
         LAUNCH_CHECK("colprep_kernel");
         dim3 pg((Np + 255) / 256, std::min(L, 256));
-        PROF_LAUNCH(EDM_PROF_PREP, cs, permute_kernel<<<pg, 256, 0, cs>>>(ds.data, ds.ld, L, Np, W.colmap, W.mean, W.lastdiff, W.Yp, W.lastdiff_p));
+        PROF_LAUNCH(EDM_PROF_PREP, cs, permute_kernel<<<pg, 256, 0, cs>>>(ds.data, ds.ld, L, Np, W.colmap, W.mean, W.Yp));
         LAUNCH_CHECK("permute_kernel");
-        PROF_LAUNCH(EDM_PROF_PREP, cs, stats_kernel<<<(Np + 127) / 128, 128, 0, cs>>>(W.Yp, L, Np, tau, Tp, ECAP, W.stats));
-        LAUNCH_CHECK("stats_kernel");
+        for (int l = lag_min; l <= lag_max; ++l) {
+            const int64_t so = (int64_t)(l - lag_min) * ECAP * W.Npm;
+            PROF_LAUNCH(EDM_PROF_PREP, cs,
+                        stats_kernel<<<(Np + 127) / 128, 128, 0, cs>>>(W.Yp, ds.data, ds.ld, W.colmap, Np, tau, m_lo + l,
+                                                                      L - 1 - m_hi + l, ECAP, W.stats + so, W.cflag + so));
+            LAUNCH_CHECK("stats_kernel");
+        }
     }
 
-    // ---- library blocks: kNN tables (S6-S8) then lookup + rho (S9, S10)
+    // ---- library blocks: kNN tables (S6-S8) then one lookup + rho pass per lag (S9, S10)
     const size_t tile_smem = (size_t)L * TILE_J * sizeof(float);
     const bool use_smem = tile_smem + lookup_ring_bytes() <= (size_t)LOOKUP_SMEM_MAX;
     const size_t lk_smem = (use_smem ? tile_smem : 0) + lookup_ring_bytes();
@@ -412,13 +420,13 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int3
     for (int r0 = 0; r0 < nlib; r0 += CCM_B) {
         const int nb = std::min(CCM_B, nlib - r0);
         KnnParams P{};
-        P.X = W.Xs; P.ldx = L; P.slot_series = W.slot_series + r0;
-        P.L = L; P.tau = tau; P.Tp = Tp; P.excl = exclude_self ? 1 : 0;
+        P.X = W.Xs + m_lo; P.ldx = L; P.slot_series = W.slot_series + r0;
+        P.L = Lk; P.tau = tau; P.Tp = m_hi; P.store_shift = 0; P.excl = exclude_self ? 1 : 0;
         P.maskS = maskS; P.Etop = Etop;
         P.slotE = (mode == EDM_E_LIBRARY) ? W.slotE + r0 : nullptr;
         P.tables = W.tables; P.T_lib = T_lib;
         memcpy(P.offE, offE, sizeof(offE));
-        st = launch_knn<MODE_CCM>(P, L - Tp, nb, cs);
+        st = launch_knn<MODE_CCM>(P, Lk - m_hi, nb, cs);
         if (st != EDM_OK) return st;
         {
             WeightParams WP{};
@@ -426,28 +434,72 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int3
             WP.slotE = (mode == EDM_E_LIBRARY) ? W.slotE + r0 : nullptr;
             memcpy(WP.offE, offE, sizeof(offE));
             int acc = 0;
-            for (int E = 1; E <= ECAP + 1; ++E) {
-                WP.rowStart[E] = acc;
-                if (E <= ECAP && ((maskS >> E) & 1u)) acc += (int)std::max<int64_t>(n_rows(L, E, tau, Tp), 0);
+            for (int Ev = 1; Ev <= ECAP + 1; ++Ev) {
+                WP.rowStart[Ev] = acc;
+                if (Ev <= ECAP && ((maskS >> Ev) & 1u)) acc += (int)std::max<int64_t>(n_rows(Lk, Ev, tau, m_hi), 0);
             }
             WP.rowStart[0] = 0;
             const int64_t nthr = (int64_t)acc * nb;
             PROF_LAUNCH(EDM_PROF_CCM_KNN, cs, weights_kernel<<<(unsigned)((nthr + 255) / 256), 256, 0, cs>>>(WP));
             LAUNCH_CHECK("weights_kernel");
         }
-        LookupParams Q{};
-        Q.Yp = W.Yp; Q.Np = Np; Q.colmap = W.colmap;
-        Q.tileE = (mode == EDM_E_TARGET) ? W.tileE : nullptr;
-        Q.slotE = W.slotE + r0; Q.slotRow = W.slot_row + r0;
-        Q.tables = W.tables; Q.T_lib = T_lib;
-        memcpy(Q.offE, offE, sizeof(offE));
-        Q.stats = W.stats; Q.lastdiff = W.lastdiff_p;
-        Q.L = L; Q.tau = tau; Q.Tp = Tp; Q.B = nb; Q.N = N; Q.rho = rho;
-        if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
-        else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
-        LAUNCH_CHECK("lookup_kernel");
+        for (int l = lag_min; l <= lag_max; ++l) {
+            LookupParams Q{};
+            Q.Yp = W.Yp; Q.Np = Np; Q.colmap = W.colmap;
+            Q.tileE = (mode == EDM_E_TARGET) ? W.tileE : nullptr;
+            Q.slotE = W.slotE + r0; Q.slotRow = W.slot_row + r0;
+            Q.tables = W.tables; Q.T_lib = T_lib;
+            memcpy(Q.offE, offE, sizeof(offE));
+            const int64_t so = (int64_t)(l - lag_min) * ECAP * W.Npm;
+            Q.stats = W.stats + so; Q.cflag = W.cflag + so;
+            Q.Lt = L; Q.Lk = Lk; Q.hrz = m_hi; Q.gshift = m_lo + l; Q.oshift = m_lo + l;
+            Q.tau = tau; Q.B = nb; Q.N = N;
+            Q.rho = rho; Q.rstride = (int64_t)nlag * N; Q.roff = (int64_t)(l - lag_min) * N;
+            if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+            else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+            LAUNCH_CHECK("lookup_kernel");
+        }
     }
     return EDM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int32_t Tp, edm_e_mode mode,
+                             int32_t exclude_self, int32_t lib_begin, int32_t lib_end, float* rho, void* workspace,
+                             size_t ws_bytes, void* stream) {
+    if (!ds.data || !E || !rho || !workspace) return fail(EDM_EINVAL, "null pointer");
+    if (ds.N < 1 || ds.L < 2 || ds.ld < ds.N || tau < 1 || Tp < 0 || (mode != EDM_E_TARGET && mode != EDM_E_LIBRARY))
+        return fail(EDM_EINVAL, "bad arguments N=%d L=%d ld=%lld tau=%d Tp=%d mode=%d", ds.N, ds.L, (long long)ds.ld, tau, Tp, (int)mode);
+    if (lib_begin < 0 || lib_end > ds.N || lib_begin > lib_end) return fail(EDM_EINVAL, "bad library range [%d,%d)", lib_begin, lib_end);
+    const size_t need = edm_workspace_bytes(1, ds.N, ds.L, ECAP, tau, Tp);
+    return ccm_core(ds, E, tau, 0, Tp, Tp, Tp, mode, exclude_self, lib_begin, lib_end, rho, workspace, ws_bytes, need,
+                    (cudaStream_t)stream);
+}
+
+size_t edm_ccm_lagged_workspace_bytes(int32_t N, int32_t L, int32_t tau, int32_t lag_min, int32_t lag_max) {
+    if (N < 1 || L < 2 || tau < 1 || lag_min > lag_max) return 0;
+    const int m_lo = lag_min < 0 ? -lag_min : 0, m_hi = lag_max > 0 ? lag_max : 0;
+    if (m_lo + m_hi >= L) return 0;
+    return ccm_ws(nullptr, N, L, L - m_lo, tau, m_hi, lag_max - lag_min + 1).bytes;
+}
+
+edm_status edm_ccm_lagged(edm_dataset ds, const int32_t* E, int32_t tau, int32_t lag_min, int32_t lag_max,
+                          edm_e_mode mode, int32_t exclude_self, int32_t lib_begin, int32_t lib_end, float* rho,
+                          void* workspace, size_t ws_bytes, void* stream) {
+    if (!ds.data || !E || !rho || !workspace) return fail(EDM_EINVAL, "null pointer");
+    if (ds.N < 1 || ds.L < 2 || ds.ld < ds.N || tau < 1 || lag_min > lag_max ||
+        (mode != EDM_E_TARGET && mode != EDM_E_LIBRARY))
+        return fail(EDM_EINVAL, "bad arguments N=%d L=%d ld=%lld tau=%d lags [%d,%d] mode=%d", ds.N, ds.L,
+                    (long long)ds.ld, tau, lag_min, lag_max, (int)mode);
+    if (lib_begin < 0 || lib_end > ds.N || lib_begin > lib_end) return fail(EDM_EINVAL, "bad library range [%d,%d)", lib_begin, lib_end);
+    const int m_lo = lag_min < 0 ? -lag_min : 0, m_hi = lag_max > 0 ? lag_max : 0;
+    if (m_lo + m_hi >= ds.L) return fail(EDM_ETOOSHORT, "lag range [%d,%d] leaves no points at L=%d", lag_min, lag_max, ds.L);
+    const size_t need = edm_ccm_lagged_workspace_bytes(ds.N, ds.L, tau, lag_min, lag_max);
+    return ccm_core(ds, E, tau, m_lo, m_hi, lag_min, lag_max, mode, exclude_self, lib_begin, lib_end, rho, workspace,
+                    ws_bytes, need, (cudaStream_t)stream);
 }
 
 edm_status edm_causal_map_host(const float* host_data, int32_t N, int32_t L, int32_t E_max, int32_t tau, int32_t Tp,

@@ -27,7 +27,8 @@ EDM_E_TARGET, EDM_E_LIBRARY = 0, 1
 E_CAP = 20
 
 EXPORTS = ("edm_embed_knn", "edm_simplex_optimal_E", "edm_ccm_all_pairs", "edm_workspace_bytes",
-           "edm_causal_map_host", "edm_last_error", "edm_version", "edm_profile_begin", "edm_profile_end")
+           "edm_causal_map_host", "edm_last_error", "edm_version", "edm_profile_begin", "edm_profile_end",
+           "edm_ccm_lagged", "edm_ccm_lagged_workspace_bytes")
 PROF_KINDS = ("prep", "simplex_knn", "simplex_rho", "ccm_knn", "lookup", "other")
 
 
@@ -68,6 +69,10 @@ def load(path: Optional[str] = None):
     lib.edm_last_error.argtypes = []
     lib.edm_version.restype = C.c_char_p
     lib.edm_version.argtypes = []
+    lib.edm_ccm_lagged.restype = i32
+    lib.edm_ccm_lagged.argtypes = [edm_dataset, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp, sz, vp]
+    lib.edm_ccm_lagged_workspace_bytes.restype = sz
+    lib.edm_ccm_lagged_workspace_bytes.argtypes = [i32, i32, i32, i32, i32]
     lib.edm_profile_begin.restype = i32
     lib.edm_profile_begin.argtypes = []
     lib.edm_profile_end.restype = i32
@@ -178,6 +183,34 @@ def ccm_all_pairs(data: torch.Tensor, E: torch.Tensor, tau: int = 1, Tp: int = 1
     ws = workspace(1, ds.N, ds.L, E_CAP, tau, Tp, data.device)
     _check(load().edm_ccm_all_pairs(ds, E.data_ptr(), tau, Tp, _mode(mode), int(exclude_self), lib_begin, lib_end,
                                     out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(data.device)))
+    return out
+
+
+def ccm_lagged(data: torch.Tensor, E: torch.Tensor, tau: int = 1, lag_min: int = -2, lag_max: int = 2,
+               mode="target", exclude_self: bool = True, lib_begin: int = 0, lib_end: Optional[int] = None,
+               out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Time-delay cross mapping (edm_ccm_lagged): rho [rows, nlags, N] for lags lag_min..lag_max
+    from one set of kNN tables per library block."""
+    ds = _dataset(data)
+    _require_cuda(E, torch.int32, "E")
+    E = E.contiguous()
+    if E.numel() != ds.N:
+        raise ValueError("E must have N entries")
+    lib_end = ds.N if lib_end is None else lib_end
+    rows, nlag = lib_end - lib_begin, lag_max - lag_min + 1
+    if out is None:
+        out = torch.empty((max(rows, 0), nlag, ds.N), dtype=torch.float32, device=data.device)
+    nbytes = load().edm_ccm_lagged_workspace_bytes(ds.N, ds.L, tau, lag_min, lag_max)
+    if nbytes == 0:
+        raise EdmError(EDM_EINVAL, f"bad lagged workspace request N={ds.N} L={ds.L} lags=[{lag_min},{lag_max}]")
+    key = ("lagged", torch.device(data.device))
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() < nbytes:
+        _ws_cache.pop(key, None)
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=data.device)
+        _ws_cache[key] = ws
+    _check(load().edm_ccm_lagged(ds, E.data_ptr(), tau, lag_min, lag_max, _mode(mode), int(exclude_self), lib_begin,
+                                 lib_end, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(data.device)))
     return out
 
 

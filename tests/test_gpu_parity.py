@@ -249,3 +249,33 @@ def test_c5_long_series_sampled():
     rows = libccm.ccm_all_pairs(d, dev(forced, torch.int32), 1, 1, "target", True, 3, 5).cpu().numpy()
     ref = O.ccm_rows(data, forced, 1, 1, 0, True, 3, 5)
     assert_rho_close(rows, ref)
+
+
+# ---------------------------------------------------------------- edm_ccm_lagged
+def test_lagged_parity_and_single_lag_identity():
+    data = synth.random_dataset(45, 160, 21)
+    rng = np.random.default_rng(5)
+    E = rng.integers(1, 7, 45).astype(np.int32)
+    d, Ed = dev(data), dev(E, torch.int32)
+    for mode in ("target", "library"):
+        g = libccm.ccm_lagged(d, Ed, 1, -3, 2, mode, True, 4, 40).cpu().numpy()
+        ref = O.ccm_lagged_rows(data, E, 1, -3, 2, 0 if mode == "target" else 1, True, 4, 40)
+        assert_rho_close(g, ref)
+        for Tp in (0, 1):
+            a = libccm.ccm_lagged(d, Ed, 1, Tp, Tp, mode).cpu().numpy()[:, 0, :]
+            b = libccm.ccm_all_pairs(d, Ed, 1, Tp, mode).cpu().numpy()
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_lagged_c3_shape_sampled_and_causal_lag():
+    data = synth.make_config("c3", N=2048)
+    d = dev(data)
+    optE = libccm.simplex_optimal_E(d, 20).cpu().numpy()
+    g = libccm.ccm_lagged(d, dev(optE, torch.int32), 1, -2, 2, "target", True, 256, 512).cpu().numpy()
+    pick = [0, 101, 255]
+    ref = np.concatenate([O.ccm_lagged_rows(data, optE, 1, -2, 2, 0, True, 256 + p, 257 + p) for p in pick])
+    assert_rho_close(g[pick], ref)
+    from tests.test_oracle_lagged import delayed_pair
+    pair = delayed_pair(1000, 3)
+    r = libccm.ccm_lagged(dev(pair), dev(np.array([2, 2]), torch.int32), 1, -6, 3).cpu().numpy()
+    assert -6 + int(np.argmax(r[1, :, 0])) == -4
