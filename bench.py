@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None, help="oracle sample size (library rows)")
+    ap.add_argument("--lags", default=None, help="time-delay cross mapping over lags A:B (SURVEY 8(f) f1) "
+                                                 "instead of the single-horizon map")
     return ap.parse_args()
 
 
@@ -144,7 +146,7 @@ def load_traffic():
 
 
 # ------------------------------------------------------------------ oracle (cpu_baseline / reference arm)
-def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series):
+def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None):
     """Time the fp64 oracle, as it stands, on a bounded sample of the same workload:
     phase 1 for n_series series and phase 2 for n_lib library rows x all N targets.
     Returns (pairs/s extrapolated to the whole workload, seconds, cores, description)."""
@@ -154,13 +156,17 @@ def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series):
     t0 = time.perf_counter()
     O.simplex_all(data, 20, tau, 0, n_series, cores)
     t1 = time.perf_counter()
-    O.ccm_rows(data, E, tau, Tp, 0 if mode == "target" else 1, True, 0, n_lib, False, cores)
+    if lags:
+        O.ccm_lagged_rows(data, E, tau, lags[0], lags[1], 0 if mode == "target" else 1, True, 0, n_lib, cores)
+    else:
+        O.ccm_rows(data, E, tau, Tp, 0 if mode == "target" else 1, True, 0, n_lib, False, cores)
     t2 = time.perf_counter()
     # whole-workload time estimate = phase-1 time x N/n_series + phase-2 time x N/n_lib
     full = (t1 - t0) * N / n_series + (t2 - t1) * N / n_lib
     desc = (f"oracle phase 1 on {n_series} series ({t1 - t0:.1f} s) + phase 2 on {n_lib} library rows x {N} "
             f"targets ({t2 - t1:.1f} s), {cores} threads; value = N^2 / (extrapolated full-map time {full:.0f} s)")
-    return N * N / full, t2 - t0, cores, desc
+    nlag = (lags[1] - lags[0] + 1) if lags else 1
+    return N * N * nlag / full, t2 - t0, cores, desc
 
 
 def run_reference(args):
@@ -240,9 +246,10 @@ def main():
     s0, s1 = distributed.shard(N, rank, world)
     l0, l1 = s0, s1
     per = -(-N // world)
-    rho_rows = torch.empty((per, N), dtype=torch.float32, device=dev)
-    gather_list = [torch.empty((per, N), dtype=torch.float32, device=dev) for _ in range(world)] \
-        if (rank == 0 and world > 1) else None
+    lags = tuple(int(v) for v in args.lags.split(":")) if args.lags else None
+    nlag = (lags[1] - lags[0] + 1) if lags else 1
+    rho_rows = torch.empty((per, nlag, N) if lags else (per, N), dtype=torch.float32, device=dev)
+    gather_list = [torch.empty_like(rho_rows) for _ in range(world)] if (rank == 0 and world > 1) else None
     Ebuf = torch.zeros(per, dtype=torch.int32, device=dev)
     Eall = torch.empty(per * world, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -262,7 +269,10 @@ def main():
             E = Ebuf[:N]
         if ev:
             ev[2].record(stream)
-        libccm.ccm_all_pairs(data, E, tau, Tp, args.mode, True, l0, l1, out=rho_rows)  # S5-S9
+        if lags:
+            libccm.ccm_lagged(data, E, tau, lags[0], lags[1], args.mode, True, l0, l1, out=rho_rows)  # f1
+        else:
+            libccm.ccm_all_pairs(data, E, tau, Tp, args.mode, True, l0, l1, out=rho_rows)  # S5-S9
         if ev:
             ev[3].record(stream)
         if world > 1:
@@ -313,14 +323,14 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_per_step = ms_total / args.steps
-    pairs = float(N) * N
+    pairs = float(N) * N * nlag
     value = pairs / (ms_per_step / 1e3)
 
     # ---- roofline of the dominant kernel (lookup) from live CUDA-event launch times
     lk_ms, lk_n = prof["lookup"]
     kn_ms, kn_n = prof["ccm_knn"]
     rows_frac = (l1 - l0) / N
-    smem_bytes_step = lookup_smem_bytes(E_host, L, tau, Tp, args.mode) * rows_frac
+    smem_bytes_step = lookup_smem_bytes(E_host, L, tau, Tp, args.mode) * rows_frac * nlag
     bytes_per_launch = smem_bytes_step * args.steps / max(lk_n, 1)
     avg_launch_s = lk_ms / max(lk_n, 1) / 1e3
     peaks = load_peaks()
@@ -367,7 +377,7 @@ def main():
 
     # ---- end to end through the public API: pinned host input -> H2D -> both phases -> D2H of rho
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and not lags:
         Bi = N * L * 4 * world
         Bo = N * N * 4
         if world == 1:
@@ -406,13 +416,15 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_lib = args.cpu_sample or min(N, 128)
-        v, secs, cores, desc = oracle_sample(host, E_host, args.mode, tau, Tp, n_lib, min(N, 256))
-        cpu = {"value": v, "unit": "pairs/s", "cores": cores, "kind": "oracle", "sample": desc}
+        v, secs, cores, desc = oracle_sample(host, E_host, args.mode, tau, Tp, n_lib, min(N, 256), lags)
+        cpu = {"value": v, "unit": "pairs/s" if not lags else "(pair, lag)/s", "cores": cores, "kind": "oracle",
+               "sample": desc}
 
     if rank == 0:
         hist = np.bincount(E_host, minlength=E_max + 1)[1:].tolist()
         out = {
-            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if not lags else f"time-delay CCM (pair, lag) cross maps/sec, lags {lags[0]}..{lags[1]}",
+            "value": value, "unit": "pairs/s" if not lags else "(pair, lag)/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64 kNN / f32 lookup", "data": "synthetic",
             "config": {"workload": f"{args.config}: {N} series x L={L}, E=1..{E_max}, tau={tau}, Tp={Tp}, "
