@@ -465,3 +465,174 @@ int oracle_ccm_lagged_rows(const float *data, int N, int L, long ld, const int *
     J.begin = lib_begin; J.end = lib_end; J.rho = rho;
     return run_pool(&J, lagged_worker, nthreads);
 }
+
+/* ---------------------------------------------------------------- CCM convergence test */
+/* SURVEY 8(f) f2 / PAPER.md P:351-356 ("in the original definition of CCM, predictions are
+ * made multiple times using randomly subsampled library sets of different sizes and it is
+ * tested whether increasing the library set size improves the prediction accuracy").
+ * Reading R16: the random draws are inputs -- R orders perm[r][0..L-1], each a
+ * permutation of the time labels. For size l and sample r the library set of dimension E is
+ *   C = the first min(l, n_E) labels of perm[r] that lie in P_E = [(E-1)tau, L-1-Tp]
+ * (a uniformly random subset of P_E, nested in l). Every t in P_E is still predicted, from its
+ * E+1 nearest neighbours in C \ {t} (exclude_self), and rho_r = Pearson over P_E as in C10.
+ * If |C| - exclude_self < E+1 the sample is undefined (NaN). The same library sets serve every
+ * (library, target) pair, so one table per (library, E, l, r) is reused for all targets. */
+
+/* C of size min(l, n_E), in perm order; returns its size. */
+static int library_subset(const int *perm, int L, int lo, int hi, int l, int *C) {
+    int n = 0;
+    for (int i = 0; i < L && n < l; ++i)
+        if (perm[i] >= lo && perm[i] <= hi) C[n++] = perm[i];
+    return n;
+}
+
+/* kNN of queries t in [qlo, qhi] of x among the candidate labels C[0..nC) (C4 over the list);
+ * returns rows, or OR_ETOOSHORT if a row has fewer than k candidates. */
+static int knn_list(const double *x, int qlo, int qhi, const int *C, int nC, int E, int tau, int excl,
+                    int *idx, double *d2) {
+    const int k = E + 1;
+    topk_t q;
+    q.k = k;
+    q.d2 = (double *)malloc(sizeof(double) * k);
+    q.s = (int *)malloc(sizeof(int) * k);
+    if (!q.d2 || !q.s) { free(q.d2); free(q.s); return OR_ENOMEM; }
+    int rc = qhi - qlo + 1;
+    for (int t = qlo; t <= qhi; ++t) {
+        q.n = 0;
+        for (int c = 0; c < nC; ++c) {
+            if (excl && C[c] == t) continue;
+            topk_push(&q, oracle_dist2(x, t, x, C[c], E, tau), C[c]);
+        }
+        if (q.n < k) { rc = OR_ETOOSHORT; break; }
+        for (int j = 0; j < k; ++j) {
+            idx[(size_t)(t - qlo) * k + j] = q.s[j];
+            d2[(size_t)(t - qlo) * k + j] = q.d2[j];
+        }
+    }
+    free(q.d2); free(q.s);
+    return rc;
+}
+
+typedef struct {
+    job_t base;
+    const int *sizes; int nsizes;
+    const int *perms; int R;
+    double *rho_mean, *rho_samples;
+} conv_job_t;
+
+/* rho_samples[((row*nsizes + q)*R + r)*N + j]; rho_mean[(row*nsizes + q)*N + j] = mean over r
+ * (ascending) of the non-NaN samples, NaN if none. */
+static int convergence_row(const conv_job_t *CJ, int i, double *x, double *y, int row) {
+    const job_t *J = &CJ->base;
+    const int L = J->L, tau = J->tau, Tp = J->Tp, N = J->N, R = CJ->R;
+    int Ecap = J->E[i];
+    for (int j = 0; j < N; ++j) if (J->E[j] > Ecap) Ecap = J->E[j];
+    int **tidx = (int **)calloc(Ecap + 1, sizeof(int *));
+    double **tw = (double **)calloc(Ecap + 1, sizeof(double *));
+    int *ok = (int *)calloc(Ecap + 1, sizeof(int));
+    int *C = (int *)malloc(sizeof(int) * L);
+    double *d2 = (double *)malloc(sizeof(double) * (size_t)L * (Ecap + 1));
+    double *p = (double *)malloc(sizeof(double) * L);
+    double *o = (double *)malloc(sizeof(double) * L);
+    double *smp = (double *)malloc(sizeof(double) * (size_t)R * N);
+    int rc = OR_OK;
+    if (!tidx || !tw || !ok || !C || !d2 || !p || !o || !smp) { rc = OR_ENOMEM; goto done; }
+    for (int E = 1; E <= Ecap; ++E) {
+        tidx[E] = (int *)malloc(sizeof(int) * (size_t)L * (E + 1));
+        tw[E] = (double *)malloc(sizeof(double) * (size_t)L * (E + 1));
+        if (!tidx[E] || !tw[E]) { rc = OR_ENOMEM; goto done; }
+    }
+    load_series(J->data, J->ld, L, i, x);
+    for (int q = 0; q < CJ->nsizes; ++q) {
+        for (int r = 0; r < R; ++r) {
+            const int *perm = CJ->perms + (size_t)r * L;
+            for (int E = 1; E <= Ecap; ++E) ok[E] = -1;  /* table of this (l, r) not built yet */
+            for (int j = 0; j < N; ++j) {
+                const int E = (J->mode == 0) ? J->E[j] : J->E[i];
+                const int k = E + 1, lo = (E - 1) * tau, hi = L - 1 - Tp, n = hi - lo + 1;
+                if (ok[E] < 0) {
+                    const int nC = library_subset(perm, L, lo, hi, CJ->sizes[q], C);
+                    ok[E] = (nC - (J->excl ? 1 : 0) >= k);
+                    if (ok[E]) {
+                        int rr = knn_list(x, lo, hi, C, nC, E, tau, J->excl, tidx[E], d2);
+                        if (rr < 0) { rc = rr; goto done; }
+                        for (int t = 0; t < n; ++t) oracle_weights(d2 + (size_t)t * k, k, tw[E] + (size_t)t * k);
+                    }
+                }
+                double rho = NAN;
+                if (ok[E]) {
+                    load_series(J->data, J->ld, L, j, y);
+                    rho = oracle_xmap(tidx[E], tw[E], n, k, lo, y, Tp, p, o);
+                }
+                smp[(size_t)r * N + j] = rho;
+            }
+        }
+        for (int j = 0; j < N; ++j) {
+            double s = 0.0;
+            int cnt = 0;
+            for (int r = 0; r < R; ++r) {
+                const double v = smp[(size_t)r * N + j];
+                if (!isnan(v)) { s = s + v; ++cnt; }
+            }
+            CJ->rho_mean[((size_t)row * CJ->nsizes + q) * N + j] = cnt ? s / cnt : NAN;
+        }
+        if (CJ->rho_samples)
+            memcpy(CJ->rho_samples + ((size_t)row * CJ->nsizes + q) * R * N, smp, sizeof(double) * (size_t)R * N);
+    }
+done:
+    if (tidx) for (int E = 0; E <= Ecap; ++E) free(tidx[E]);
+    if (tw) for (int E = 0; E <= Ecap; ++E) free(tw[E]);
+    free(tidx); free(tw); free(ok); free(C); free(d2); free(p); free(o); free(smp);
+    return rc;
+}
+
+static void *convergence_worker(void *arg) {
+    conv_job_t *CJ = (conv_job_t *)arg;
+    job_t *J = &CJ->base;
+    double *x = (double *)malloc(sizeof(double) * J->L);
+    double *y = (double *)malloc(sizeof(double) * J->L);
+    if (!x || !y) { J->err = OR_ENOMEM; free(x); free(y); return NULL; }
+    for (;;) {
+        int r = __sync_fetch_and_add(&J->next, 1);
+        if (r >= J->end - J->begin || J->err) break;
+        int rc = convergence_row(CJ, J->begin + r, x, y, r);
+        if (rc != OR_OK) J->err = rc;
+    }
+    free(x); free(y);
+    return NULL;
+}
+
+int oracle_ccm_convergence_rows(const float *data, int N, int L, long ld, const int *E, int tau, int Tp,
+                                int mode, int exclude_self, const int *sizes, int nsizes, const int *perms,
+                                int R, int lib_begin, int lib_end, double *rho_mean, double *rho_samples,
+                                int nthreads) {
+    if (!data || !E || !sizes || !perms || !rho_mean || N < 1 || L < 2 || tau < 1 || Tp < 0 ||
+        nsizes < 1 || R < 1 || lib_begin < 0 || lib_end > N || lib_begin > lib_end || (mode != 0 && mode != 1))
+        return OR_EINVAL;
+    for (int q = 0; q < nsizes; ++q) if (sizes[q] < 1) return OR_EINVAL;
+    char *seen = (char *)malloc(L);
+    if (!seen) return OR_ENOMEM;
+    for (int r = 0; r < R; ++r) {  /* every order is a permutation of 0..L-1 */
+        memset(seen, 0, L);
+        for (int i = 0; i < L; ++i) {
+            const int v = perms[(size_t)r * L + i];
+            if (v < 0 || v >= L || seen[v]) { free(seen); return OR_EINVAL; }
+            seen[v] = 1;
+        }
+    }
+    free(seen);
+    for (int j = 0; j < N; ++j) {
+        if (E[j] < 1) return OR_EINVAL;
+        int n = L - (E[j] - 1) * tau - Tp;
+        if (n - (exclude_self ? 1 : 0) < E[j] + 1) return OR_ETOOSHORT;
+    }
+    conv_job_t CJ;
+    memset(&CJ, 0, sizeof(CJ));
+    job_t *J = &CJ.base;
+    J->data = data; J->N = N; J->L = L; J->ld = ld; J->E = E; J->tau = tau; J->Tp = Tp;
+    J->mode = mode; J->excl = exclude_self;
+    J->begin = lib_begin; J->end = lib_end;
+    CJ.sizes = sizes; CJ.nsizes = nsizes; CJ.perms = perms; CJ.R = R;
+    CJ.rho_mean = rho_mean; CJ.rho_samples = rho_samples;
+    return run_pool((job_t *)&CJ, convergence_worker, nthreads);
+}

@@ -61,6 +61,9 @@ def lib():
         _lib.oracle_ccm_rows.argtypes = [fp, i, i, C.c_long, ip, i, i, i, i, i, i, i, dp, i]
         _lib.oracle_ccm_lagged_rows.restype = i
         _lib.oracle_ccm_lagged_rows.argtypes = [fp, i, i, C.c_long, ip, i, i, i, i, i, i, i, dp, i]
+        _lib.oracle_ccm_convergence_rows.restype = i
+        _lib.oracle_ccm_convergence_rows.argtypes = [fp, i, i, C.c_long, ip, i, i, i, i, ip, i, ip, i, i, i, dp, dp,
+                                                     i]
     return _lib
 
 
@@ -207,3 +210,28 @@ def ccm_lagged_rows(data, E, tau=1, lag_min=-2, lag_max=2, mode=MODE_TARGET, exc
                                         lib_end, rho.ctypes.data_as(C.POINTER(C.c_double)),
                                         nthreads or nthreads_default()), "ccm_lagged_rows")
     return rho
+
+
+def ccm_convergence_rows(data, E, sizes, perms, tau=1, Tp=1, mode=MODE_TARGET, exclude_self=True, lib_begin=0,
+                         lib_end=None, samples=False, nthreads=None):
+    """CCM convergence test (reading R16): for every library size
+    sizes[q] and random order perms[r] (permutations of 0..L-1), the cross-map skill with the
+    library set = the first min(l, n_E) labels of perms[r] inside P_E. Returns the mean over r of
+    the non-NaN samples, rho [rows, nsizes, N] fp64, and (samples=True) also every sample
+    [rows, nsizes, R, N]."""
+    data, pd = _f(data)
+    L, N = data.shape
+    E, pe = _i(E)
+    sizes, psz = _i(sizes)
+    perms, pp = _i(np.atleast_2d(perms))
+    R = perms.shape[0]
+    assert perms.shape[1] == L
+    lib_end = N if lib_end is None else lib_end
+    rows = lib_end - lib_begin
+    mean = np.zeros((rows, len(sizes), N), np.float64)
+    smp = np.zeros((rows, len(sizes), R, N), np.float64) if samples else None
+    _check(lib().oracle_ccm_convergence_rows(pd, N, L, N, pe, tau, Tp, mode, int(exclude_self), psz, len(sizes), pp, R,
+                                             lib_begin, lib_end, mean.ctypes.data_as(C.POINTER(C.c_double)),
+                                             smp.ctypes.data_as(C.POINTER(C.c_double)) if samples else None,
+                                             nthreads or nthreads_default()), "ccm_convergence_rows")
+    return (mean, smp) if samples else mean

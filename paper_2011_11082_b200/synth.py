@@ -135,3 +135,11 @@ def random_dataset(N: int, L: int, seed: int) -> np.ndarray:
     q = quantise8(d)
     d[:, ::4] = q[:, ::4]
     return np.ascontiguousarray(d)
+
+
+def library_orders(R: int, L: int, seed: int) -> np.ndarray:
+    """R seeded random orders of the time labels 0..L-1, int32 [R, L]: the random draws of the
+    CCM convergence test (R16). Sample r's library set of size l is the first l labels
+    of row r inside the row set P_E."""
+    rng = np.random.default_rng(seed)
+    return np.stack([rng.permutation(L) for _ in range(R)]).astype(np.int32)
