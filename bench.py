@@ -42,10 +42,14 @@ def parse():
     ap.add_argument("--impl", default="libccm", choices=["libccm", "reference"])
     ap.add_argument("--config", default="c3", choices=list(synth.CONFIGS))
     ap.add_argument("--N", type=int, default=None, help="override N (smaller runs of the same recipe)")
+    ap.add_argument("--L", type=int, default=None, help="override L (long-series runs of the same recipe)")
     ap.add_argument("--mode", default="target", choices=["target", "library"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None, help="oracle sample size (library rows)")
+    ap.add_argument("--convergence", default=None,
+                    help="CCM convergence test (SURVEY 8(f) f2) over comma-separated library sizes, e.g. 50,200,999")
+    ap.add_argument("--samples", type=int, default=4, help="random library sets per size (--convergence)")
     ap.add_argument("--lags", default=None, help="time-delay cross mapping over lags A:B (SURVEY 8(f) f1) "
                                                  "instead of the single-horizon map")
     return ap.parse_args()
@@ -114,15 +118,16 @@ def lookup_smem_bytes(E: np.ndarray, L: int, tau: int, Tp: int, mode: str) -> fl
     return float(N * per_target.sum())               # library mode: row i uses E_i for all N targets
 
 
-def knn_fp64_ops(E: np.ndarray, L: int, tau: int, Tp: int, mode: str) -> float:
+def knn_fp64_ops(E: np.ndarray, L: int, tau: int, Tp: int, mode: str, lib_size: int | None = None) -> float:
     """Algorithmic fp64 operations of the phase-2 distance pass: for each library, every
     ordered pair (t, s != t) of P_E at every E up to the largest needed E costs one
-    subtract, multiply and add (incremental over E)."""
+    subtract, multiply and add (incremental over E). With a library set of size
+    lib_size (convergence test) the candidates per query are min(lib_size, n_E)."""
     def per_lib(etop):
         tot = 0.0
         for e in range(1, etop + 1):
             n = L - (e - 1) * tau - Tp
-            tot += n * (n - 1) * 3.0
+            tot += n * ((n if lib_size is None else min(lib_size, n)) - 1) * 3.0
         return tot
     if mode == "target":
         return len(E) * per_lib(int(E.max()))
@@ -146,7 +151,7 @@ def load_traffic():
 
 
 # ------------------------------------------------------------------ oracle (cpu_baseline / reference arm)
-def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None):
+def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None, conv=None):
     """Time the fp64 oracle, as it stands, on a bounded sample of the same workload:
     phase 1 for n_series series and phase 2 for n_lib library rows x all N targets.
     Returns (pairs/s extrapolated to the whole workload, seconds, cores, description)."""
@@ -158,6 +163,9 @@ def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None):
     t1 = time.perf_counter()
     if lags:
         O.ccm_lagged_rows(data, E, tau, lags[0], lags[1], 0 if mode == "target" else 1, True, 0, n_lib, cores)
+    elif conv:
+        O.ccm_convergence_rows(data, E, conv[0], conv[1], tau, Tp, 0 if mode == "target" else 1, True, 0, n_lib,
+                               nthreads=cores)
     else:
         O.ccm_rows(data, E, tau, Tp, 0 if mode == "target" else 1, True, 0, n_lib, False, cores)
     t2 = time.perf_counter()
@@ -165,7 +173,7 @@ def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None):
     full = (t1 - t0) * N / n_series + (t2 - t1) * N / n_lib
     desc = (f"oracle phase 1 on {n_series} series ({t1 - t0:.1f} s) + phase 2 on {n_lib} library rows x {N} "
             f"targets ({t2 - t1:.1f} s), {cores} threads; value = N^2 / (extrapolated full-map time {full:.0f} s)")
-    nlag = (lags[1] - lags[0] + 1) if lags else 1
+    nlag = (lags[1] - lags[0] + 1) if lags else (len(conv[0]) * len(conv[1]) if conv else 1)
     return N * N * nlag / full, t2 - t0, cores, desc
 
 
@@ -175,7 +183,7 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = synth.CONFIGS[args.config]
-    data = synth.make_config(args.config, N=args.N)
+    data = synth.make_config(args.config, N=args.N, L=args.L)
     L, N = data.shape
     from oracle import oracle as O
     n_series = min(N, 64)
@@ -237,7 +245,7 @@ def main():
 
     cfg = synth.CONFIGS[args.config]
     E_max, tau, Tp = cfg["E_max"], cfg["tau"], cfg["Tp"]
-    host = synth.make_config(args.config, N=args.N)       # same seed on every rank
+    host = synth.make_config(args.config, N=args.N, L=args.L)  # same seed on every rank
     L, N = host.shape
     host_pinned = torch.from_numpy(host).pin_memory()
     data = host_pinned.to(dev, non_blocking=True)          # every GPU holds the full dataset (8(e))
@@ -248,6 +256,11 @@ def main():
     per = -(-N // world)
     lags = tuple(int(v) for v in args.lags.split(":")) if args.lags else None
     nlag = (lags[1] - lags[0] + 1) if lags else 1
+    conv = None
+    if args.convergence:
+        conv_sizes = [int(v) for v in args.convergence.split(",")]
+        conv = (conv_sizes, synth.library_orders(args.samples, L, synth.SEED_BASE + 7))
+        nlag = len(conv_sizes) * args.samples  # cross maps per (library, target) pair
     rho_rows = torch.empty((per, nlag, N) if lags else (per, N), dtype=torch.float32, device=dev)
     gather_list = [torch.empty_like(rho_rows) for _ in range(world)] if (rank == 0 and world > 1) else None
     Ebuf = torch.zeros(per, dtype=torch.int32, device=dev)
@@ -271,6 +284,8 @@ def main():
             ev[2].record(stream)
         if lags:
             libccm.ccm_lagged(data, E, tau, lags[0], lags[1], args.mode, True, l0, l1, out=rho_rows)  # f1
+        elif conv:
+            libccm.ccm_convergence(data, E, conv[0], conv[1], tau, Tp, args.mode, True, l0, l1)  # f2
         else:
             libccm.ccm_all_pairs(data, E, tau, Tp, args.mode, True, l0, l1, out=rho_rows)  # S5-S9
         if ev:
@@ -330,7 +345,15 @@ def main():
     lk_ms, lk_n = prof["lookup"]
     kn_ms, kn_n = prof["ccm_knn"]
     rows_frac = (l1 - l0) / N
-    smem_bytes_step = lookup_smem_bytes(E_host, L, tau, Tp, args.mode) * rows_frac * nlag
+    if conv:
+        # one lookup pass per (size l, sample) over the pairs whose E admits l (l - 1 >= E + 1):
+        # N x sum over those E of the per-target bytes (target mode: targets j, library mode: rows i)
+        def conv_bytes(l):
+            sub = E_host[E_host <= l - 2]
+            return lookup_smem_bytes(sub, L, tau, Tp, args.mode) * N / len(sub) if len(sub) else 0.0
+        smem_bytes_step = sum(conv_bytes(l) for l in conv[0]) * args.samples * rows_frac
+    else:
+        smem_bytes_step = lookup_smem_bytes(E_host, L, tau, Tp, args.mode) * rows_frac * nlag
     bytes_per_launch = smem_bytes_step * args.steps / max(lk_n, 1)
     avg_launch_s = lk_ms / max(lk_n, 1) / 1e3
     peaks = load_peaks()
@@ -354,7 +377,17 @@ def main():
                      "frac": (ntiles_bytes / avg_launch_s / 1e9 / hbm_peak) if lk_n else None,
                      "note": "north_star roof: HBM bytes of the staged target tiles (measured copy peak)"},
     }
-    knn_ops = knn_fp64_ops(E_host, L, tau, Tp, args.mode) * rows_frac
+    if conv:
+        def conv_ops(l):
+            sub = E_host[E_host <= l - 2]
+            if not len(sub):
+                return 0.0
+            if args.mode == "target":  # every library builds tables up to the largest admitted E
+                return knn_fp64_ops(sub[:1] * 0 + sub.max(), L, tau, Tp, "target", l) * N
+            return knn_fp64_ops(sub, L, tau, Tp, "library", l)
+        knn_ops = sum(conv_ops(l) for l in conv[0]) * args.samples * rows_frac
+    else:
+        knn_ops = knn_fp64_ops(E_host, L, tau, Tp, args.mode) * rows_frac
     fp64_peak = nsm * 64.0 * sm_max_mhz * 1e6 / 1e12  # Tops/s: 64 fp64 lanes/clk/SM (measured, tools/microbench)
     roofline_knn = {
         "kernel": "knn_kernel<CCM> (S6-S8: fp64 incremental distances + warp top-k + weights)",
@@ -377,7 +410,7 @@ def main():
 
     # ---- end to end through the public API: pinned host input -> H2D -> both phases -> D2H of rho
     e2e = None
-    if args.e2e_steps > 0 and not lags:
+    if args.e2e_steps > 0 and not lags and not conv:
         Bi = N * L * 4 * world
         Bo = N * N * 4
         if world == 1:
@@ -414,17 +447,19 @@ def main():
 
     # ---- CPU baseline: the oracle on a bounded sample, rank 0 at N=1 only
     cpu = None
+    unit = "(pair, lag)/s" if lags else "(pair, size, sample)/s" if conv else "pairs/s"
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_lib = args.cpu_sample or min(N, 128)
-        v, secs, cores, desc = oracle_sample(host, E_host, args.mode, tau, Tp, n_lib, min(N, 256), lags)
-        cpu = {"value": v, "unit": "pairs/s" if not lags else "(pair, lag)/s", "cores": cores, "kind": "oracle",
-               "sample": desc}
+        n_lib = args.cpu_sample or (min(N, 128) if not conv else min(N, max(16, 128 // nlag)))
+        v, secs, cores, desc = oracle_sample(host, E_host, args.mode, tau, Tp, n_lib, min(N, 256), lags, conv)
+        cpu = {"value": v, "unit": unit, "cores": cores, "kind": "oracle", "sample": desc}
 
     if rank == 0:
         hist = np.bincount(E_host, minlength=E_max + 1)[1:].tolist()
         out = {
-            "metric": METRIC if not lags else f"time-delay CCM (pair, lag) cross maps/sec, lags {lags[0]}..{lags[1]}",
-            "value": value, "unit": "pairs/s" if not lags else "(pair, lag)/s", "n_gpus": world, "steps": args.steps,
+            "metric": (f"time-delay CCM (pair, lag) cross maps/sec, lags {lags[0]}..{lags[1]}" if lags else
+                       f"CCM convergence test (pair, library size, sample) cross maps/sec, sizes {conv[0]}, "
+                       f"{args.samples} samples" if conv else METRIC),
+            "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64 kNN / f32 lookup", "data": "synthetic",
             "config": {"workload": f"{args.config}: {N} series x L={L}, E=1..{E_max}, tau={tau}, Tp={Tp}, "

@@ -125,6 +125,33 @@ edm_status edm_ccm_lagged(edm_dataset ds, const int32_t *E, int32_t tau, int32_t
                           void *workspace, size_t ws_bytes, void *stream);
 size_t edm_ccm_lagged_workspace_bytes(int32_t N, int32_t L, int32_t tau, int32_t lag_min, int32_t lag_max);
 
+/* CCM convergence test ("predictions are made multiple times using
+ * randomly subsampled library sets of different sizes and it is tested whether increasing the
+ * library set size improves the prediction accuracy"). Reading R16: the random draws
+ * are the caller's R orders of the time labels; for size l = lib_sizes[q] and sample r the
+ * library set at dimension E is
+ *   C = the first min(l, n_E) labels of orders[r] that lie in P_E = [(E-1)tau, L-1-Tp],
+ * every t in P_E is predicted from its E+1 nearest neighbours in C minus {t} (exclude_self),
+ * and the sample skill is the Pearson rho over P_E as in edm_ccm_all_pairs. The same sets serve
+ * every (library, target) pair, so each (library, E, l, r) gets one table reused for all targets.
+ *   lib_sizes   : HOST int32[n_sizes], each >= 1 (any order; sizes beyond n_E mean "all of P_E").
+ *   orders      : HOST int32[R * L], row r a permutation of 0..L-1 (EINVAL otherwise).
+ *   rho         : device float[(lib_end - lib_begin) * n_sizes * N], entry ((i - lib_begin) * n_sizes
+ *                 + q) * N + j = mean over r (ascending) of the non-NaN samples; NaN if none. A
+ *                 sample is NaN where l - exclude_self < E + 1 (too few neighbours) or as in
+ *                 edm_ccm_all_pairs (zero variance).
+ *   rho_samples : device float[(lib_end - lib_begin) * n_sizes * R * N] or NULL; entry
+ *                 (((i - lib_begin) * n_sizes + q) * R + r) * N + j = sample r.
+ *   workspace   : device scratch of at least edm_ccm_convergence_workspace_bytes.
+ * Errors as edm_ccm_all_pairs; EUNSUPPORTED if L - Tp > 58,112 (the set bitmap is staged in
+ * shared memory). Work: n_sizes * R table builds and lookup passes per library block. */
+edm_status edm_ccm_convergence(edm_dataset ds, const int32_t *E, int32_t tau, int32_t Tp, edm_e_mode mode,
+                               int32_t exclude_self, const int32_t *lib_sizes, int32_t n_sizes,
+                               const int32_t *orders, int32_t R, int32_t lib_begin, int32_t lib_end, float *rho,
+                               float *rho_samples, void *workspace, size_t ws_bytes, void *stream);
+size_t edm_ccm_convergence_workspace_bytes(int32_t N, int32_t L, int32_t tau, int32_t Tp, int32_t n_sizes,
+                                           int32_t R);
+
 /* Scratch size in bytes for which = 0 (edm_simplex_optimal_E over N series) or
  * which = 1 (edm_ccm_all_pairs over an N-series dataset; E_max = largest E in E[]).
  * Returns 0 for invalid arguments. */

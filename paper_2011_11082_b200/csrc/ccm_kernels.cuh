@@ -134,6 +134,11 @@ struct KnnParams {
     int* out_idx;
     float* out_dist;
     float* out_w;
+    // CCM convergence test (knn_kernel<..., CMASK = true): candidate s is admissible at E only if
+    // bit E-1 of allow[s] is set; clist[0..*ncl) = the ascending labels with allow != 0
+    const unsigned* allow;
+    const int* clist;
+    const int* ncl;
 };
 
 struct KnnOffsets {
@@ -272,10 +277,10 @@ __device__ __forceinline__ double list_merge(KnnWarpSmem& W, int e, unsigned bal
 // bounds the final one; the sweep filters against that bound and merges the few candidates
 // that beat it (duplicates of prefilled entries are dropped). This changes the work, not the
 // result: the final list is the k smallest keys over all candidates either way.
-template <int MODE, bool TAU1, bool FULLMASK>
+template <int MODE, bool TAU1, bool FULLMASK, bool CMASK>
 __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, unsigned* memb, int mw,
                                          const float* __restrict__ qaf, const float* __restrict__ cbf,
-                                         int t_begin, int t_end, int ncand,
+                                         int t_begin, int t_end, int ncand, int ncl,
                                          unsigned mask, int Etop, int b, int lane) {
     const int tau = TAU1 ? 1 : P.tau;
     const bool excl = (MODE != MODE_SIMPLEX) && P.excl;
@@ -298,9 +303,15 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
             const int k = e + 2;
             double* LD = W.D + loff(e);
             int* LS = W.S + loff(e);
-            const int c = (lane < k ? LS[lane] : 0) + 1;
-            const bool ok = lane < k && e < prevEq && c < ncand && c - e * tau >= 0 && !(excl && c == t);
-            const bool all = __ballot_sync(FULL, ok) == ((1u << k) - 1u);
+            const int c = (int)((unsigned)(lane < k ? LS[lane] : 0) + 1u);
+            bool ok = lane < k && e < prevEq && c < ncand && c - e * tau >= 0 && !(excl && c == t);
+            if (CMASK) ok = ok && ((__ldg(P.allow + c) >> e) & 1u);
+            const unsigned okm = __ballot_sync(FULL, ok);
+            // without a candidate mask the list is seeded only when every successor is valid;
+            // with one (sparse library sets) the valid successors seed a partial list, the
+            // missing entries being +inf keys with distinct labels
+            const bool all = CMASK ? okm != 0u : okm == ((1u << k) - 1u);
+            const int cc = ok ? c : 0x7fffffff - lane;
             double D = CUDART_INF;
             if (all && ok) {
                 D = 0.0;
@@ -314,15 +325,15 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
                 rank = 0;
                 for (int i = 0; i < k; ++i) {
                     const double Di = __shfl_sync(FULL, D, i);
-                    const int ci = __shfl_sync(FULL, c, i);
-                    rank += (Di < D || (Di == D && ci < c)) ? 1 : 0;
+                    const int ci = __shfl_sync(FULL, cc, i);
+                    rank += (Di < D || (Di == D && ci < cc)) ? 1 : 0;
                 }
             }
             __syncwarp();
             if (lane < k) {
                 LD[rank] = all ? D : CUDART_INF;
-                LS[rank] = all ? c : 0x7fffffff;
-                if (all && memb) {
+                LS[rank] = all ? cc : 0x7fffffff;
+                if (all && ok && memb) {
                     atomicOr(memb + c, 1u << e);
                     atomicOr(&W.ubits[c >> 5], 1u << (c & 31));
                 }
@@ -385,6 +396,7 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
                 }
             }
             if (memb) pass &= ~memb[s];
+            if (CMASK) pass &= __ldg(P.allow + s);  // s <= ncand: allow has ncand + 1 words
             if (__any_sync(FULL, pass != 0u)) flush(s, pass);
         };
         if (memb) {
@@ -425,8 +437,12 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
             for (int g = lane; g < nU; g += 32) memb[W.ulist[g]] = 0xffffffffu;
             __syncwarp();
         }
-        // ---- sweep over all candidates in increasing s
-        for (int c0 = 0; c0 < ncand; c0 += 32) chunk(c0 + lane);
+        // ---- sweep over all candidates in increasing s (convergence test: the library set only)
+        if (CMASK) {
+            for (int g = 0; g < ncl; g += 32) chunk(g + lane < ncl ? __ldg(P.clist + g + lane) : ncand);
+        } else {
+            for (int c0 = 0; c0 < ncand; c0 += 32) chunk(c0 + lane);
+        }
         // ---- finalise every selected E of this query
         for (int e = 0; e < Eq; ++e) {
             if (!selected(e)) continue;
@@ -464,7 +480,7 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
 // grid = (ceil(nq / KNN_QPB), slots); block = KNN_WARPS * 32; dynamic smem = knn_smem_bytes.
 // Warp w of CTA x handles the contiguous queries [x*QPB + w*QPW, +QPW) (so that each query
 // can seed its bounds from the previous one).
-template <int MODE, bool TAU1, bool FULLMASK>
+template <int MODE, bool TAU1, bool FULLMASK, bool CMASK>
 __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnParams P) {
     extern __shared__ __align__(16) unsigned char knn_smem[];
 
@@ -491,6 +507,7 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnPa
     int Etop = P.Etop;
     if (P.slotE) {
         const int e = P.slotE[b];
+        if (e > P.Etop) return;  // convergence test: no library set of this size admits E = e
         mask = 1u << e;
         Etop = e;
     }
@@ -510,7 +527,8 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnPa
     }
     const int t0 = blockIdx.x * KNN_QPB + warp * KNN_QPW;
     const int t1 = min(nq, t0 + KNN_QPW);
-    if (t0 < t1) knn_warp<MODE, TAU1, FULLMASK>(P, W, memb, mw, qaf, cbf, t0, t1, ncand, mask, Etop, b, lane);
+    const int ncl = CMASK ? __ldg(P.ncl) : 0;
+    if (t0 < t1) knn_warp<MODE, TAU1, FULLMASK, CMASK>(P, W, memb, mw, qaf, cbf, t0, t1, ncand, ncl, mask, Etop, b, lane);
 }
 
 // Weights of the phase-2 tables (S8, C5), one thread per table row: the kNN kernel
@@ -664,8 +682,9 @@ struct LookupParams {
     int Lk, hrz;            // table rows at E: n_E = Lk - (E-1) tau - hrz
     int gshift, oshift;     // gather y[label + gshift]; observe y[(E-1)tau + oshift + r]
     int tau, B, N;
-    float* rho;             // rho[slotRow * rstride + roff + col]
-    int64_t rstride, roff;
+    float* rho;             // rho[(slotRow - rbase) * rstride + roff + col]
+    int64_t rstride, roff, rbase;
+    int Eok;                // E > Eok: no table (convergence test, library set too small) -> NaN
 };
 
 // ---- per-warp table staging: TMA bulk copies (cp.async.bulk) into a 2-stage shared-memory
@@ -799,7 +818,7 @@ __device__ __forceinline__ void lookup_one(const LookupParams& P, const float* _
         const double vo = st.y - st.x * st.x / nn;
         float r = CUDART_NAN_F;
         if (!o_const && vp > 0.0 && vo > 0.0) r = (float)(cov / sqrt(vp * vo));
-        P.rho[(int64_t)P.slotRow[b] * P.rstride + P.roff + col] = r;
+        P.rho[((int64_t)P.slotRow[b] - P.rbase) * P.rstride + P.roff + col] = r;
     }
 }
 
@@ -858,8 +877,73 @@ __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupPara
     const int col = P.colmap[tile * TILE_J + lane];
     for (int b = warp; b < P.B; b += LOOKUP_WARPS) {
         const int E = P.tileE ? Et : P.slotE[b];
+        if (E > P.Eok) {
+            if (col >= 0) P.rho[((int64_t)P.slotRow[b] - P.rbase) * P.rstride + P.roff + col] = CUDART_NAN_F;
+            continue;
+        }
         lookup_dispatch(E, P, Y, ys, tile, b, lane, col, R);
     }
+}
+
+// ------------------------------------------------------------------ CCM convergence test
+// Library sets of one (size l, sample r) (reading R16): for every E in emask, the
+// first min(l, n_E) labels of the order perm[0..L) that lie in P_E = [(E-1)tau, ncand-1]
+// (ncand = L - Tp). allow[s] bit E-1 <=> s is in the set of E; clist = ascending labels with
+// allow != 0, *ncl their count. One CTA per (l, r); thread E-1 walks the order (the sets of
+// different E differ near the series start, where P_E begins).
+__global__ void subset_kernel(const int* __restrict__ perms, int L, int ncand, int tau, unsigned emask,
+                              const int* __restrict__ sizes, int R, unsigned* __restrict__ allow, int64_t allow_ld,
+                              int* __restrict__ clist, int64_t clist_ld, int* __restrict__ ncl) {
+    extern __shared__ unsigned aw[];  // [ncand]
+    const int qr = blockIdx.x, l = sizes[qr / R];
+    const int* perm = perms + (int64_t)(qr % R) * L;
+    for (int s = threadIdx.x; s < ncand; s += blockDim.x) aw[s] = 0u;
+    __syncthreads();
+    const int e = threadIdx.x;
+    if (e < ECAP && ((emask >> (e + 1)) & 1u)) {
+        const int lo = e * tau;
+        int cnt = 0;
+        for (int i = 0; i < L && cnt < l; ++i) {
+            const int s = perm[i];
+            if (s >= lo && s < ncand) {
+                atomicOr(aw + s, 1u << e);
+                ++cnt;
+            }
+        }
+    }
+    __syncthreads();
+    unsigned* al = allow + (int64_t)qr * allow_ld;
+    for (int s = threadIdx.x; s < (int)allow_ld; s += blockDim.x) al[s] = s < ncand ? aw[s] : 0u;
+    if (threadIdx.x < 32) {  // ordered compaction by warp 0
+        const int lane = threadIdx.x;
+        int* cl = clist + (int64_t)qr * clist_ld;
+        int n = 0;
+        for (int base = 0; base < ncand; base += 32) {
+            const int s = base + lane;
+            const bool in = s < ncand && aw[s] != 0u;
+            const unsigned m = __ballot_sync(FULL, in);
+            if (in) cl[n + __popc(m & ((1u << lane) - 1u))] = s;
+            n += __popc(m);
+        }
+        if (lane == 0) ncl[qr] = n;
+    }
+}
+
+// dst[i * d_stride + j] = mean over r = 0..R-1 (ascending, fp64) of the non-NaN samples
+// src[i * s_stride + r * N + j], i < nrows; NaN if every sample is NaN.
+__global__ void sample_mean_kernel(const float* __restrict__ src, int64_t s_stride, float* __restrict__ dst,
+                                   int64_t d_stride, int nrows, int R, int N) {
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= (int64_t)nrows * N) return;
+    const int i = (int)(gid / N), j = (int)(gid % N);
+    const float* p = src + (int64_t)i * s_stride + j;
+    double s = 0.0;
+    int cnt = 0;
+    for (int r = 0; r < R; ++r) {
+        const float v = p[(int64_t)r * N];
+        if (!isnan(v)) { s += (double)v; ++cnt; }
+    }
+    dst[(int64_t)i * d_stride + j] = cnt ? (float)(s / cnt) : CUDART_NAN_F;
 }
 
 }  // namespace ccm

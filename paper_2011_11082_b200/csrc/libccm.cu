@@ -179,25 +179,71 @@ CcmWs ccm_ws(void* base, int N, int L, int Lk, int tau, int hrz, int nlag) {
     return w;
 }
 
-template <int MODE, bool TAU1, bool FULL>
+// CCM convergence test (edm_ccm_convergence): the caller's sizes/orders and the per-(size,
+// sample) library sets, carved after the phase-2 workspace.
+struct ConvArgs {
+    const int32_t* sizes;   // host [nsizes]
+    int nsizes, R;
+    const int32_t* perms;   // host [R][L]
+    float* rho_samples;     // device [rows][nsizes][R][N] or NULL
+};
+struct ConvWs {
+    int* perms;        // [R][L]
+    int* sizes;        // [nsizes]
+    unsigned* allow;   // [nsizes*R][allow_ld]
+    int* clist;        // [nsizes*R][L]
+    int* ncl;          // [nsizes*R]
+    float* samples;    // [CCM_B][R][N]
+    int64_t allow_ld;
+    size_t bytes;
+};
+ConvWs conv_ws(void* base, int N, int L, int nsizes, int R) {
+    ConvWs w{};
+    size_t off = 0;
+    char* b = (char*)base;
+    auto take = [&](size_t bytes) { char* p = b + off; off += align_up(bytes); return p; };
+    const int64_t nqr = (int64_t)nsizes * R;
+    w.allow_ld = L + 32;
+    w.perms = (int*)take((size_t)R * L * sizeof(int));
+    w.sizes = (int*)take((size_t)nsizes * sizeof(int));
+    w.allow = (unsigned*)take((size_t)nqr * w.allow_ld * sizeof(unsigned));
+    w.clist = (int*)take((size_t)nqr * L * sizeof(int));
+    w.ncl = (int*)take((size_t)nqr * sizeof(int));
+    w.samples = (float*)take((size_t)CCM_B * R * N * sizeof(float));
+    w.bytes = off;
+    return w;
+}
+
+template <int MODE, bool TAU1, bool FULL, bool CMASK>
 edm_status launch_knn_t(const KnnParams& P, dim3 grid, size_t smem, cudaStream_t st) {
     if (smem > 48 * 1024)
-        CUDA_TRY(cudaFuncSetAttribute(knn_kernel<MODE, TAU1, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(cudaFuncSetAttribute(knn_kernel<MODE, TAU1, FULL, CMASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
     PROF_LAUNCH(MODE == MODE_CCM ? EDM_PROF_CCM_KNN : MODE == MODE_SIMPLEX ? EDM_PROF_SIMPLEX_KNN : EDM_PROF_OTHER, st,
-                knn_kernel<MODE, TAU1, FULL><<<grid, KNN_WARPS * 32, smem, st>>>(P));
+                knn_kernel<MODE, TAU1, FULL, CMASK><<<grid, KNN_WARPS * 32, smem, st>>>(P));
     LAUNCH_CHECK("knn_kernel");
     return EDM_OK;
 }
 
-// Picks the specialisation: tau == 1 (constant-offset shared loads) and whether every E in
-// 1..Etop is selected (no per-E membership test).
+template <int MODE, bool CMASK>
+edm_status launch_knn_m(const KnnParams& P, dim3 grid, size_t smem, bool full, cudaStream_t st) {
+    if (P.tau == 1)
+        return full ? launch_knn_t<MODE, true, true, CMASK>(P, grid, smem, st) : launch_knn_t<MODE, true, false, CMASK>(P, grid, smem, st);
+    return full ? launch_knn_t<MODE, false, true, CMASK>(P, grid, smem, st) : launch_knn_t<MODE, false, false, CMASK>(P, grid, smem, st);
+}
+
+// Picks the specialisation: tau == 1 (constant-offset shared loads), whether every E in
+// 1..Etop is selected (no per-E membership test) and (phase 2) whether a library-set mask
+// restricts the candidates (convergence test).
 template <int MODE>
 edm_status launch_knn(const KnnParams& P, int nq, int slots, cudaStream_t st) {
     dim3 grid((nq + KNN_QPB - 1) / KNN_QPB, slots);
     const size_t smem = knn_smem_bytes(P.L, P.tau);
     const bool full = !P.slotE && P.Etop >= 1 && P.maskS == ((2u << P.Etop) - 2u);
-    if (P.tau == 1) return full ? launch_knn_t<MODE, true, true>(P, grid, smem, st) : launch_knn_t<MODE, true, false>(P, grid, smem, st);
-    return full ? launch_knn_t<MODE, false, true>(P, grid, smem, st) : launch_knn_t<MODE, false, false>(P, grid, smem, st);
+    if constexpr (MODE == MODE_CCM) {
+        if (P.allow) return launch_knn_m<MODE, true>(P, grid, smem, full, st);
+    }
+    return launch_knn_m<MODE, false>(P, grid, smem, full, st);
 }
 
 }  // namespace
@@ -324,6 +370,93 @@ edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int
 
 namespace {
 
+// Weights of the rows of every E in maskS of nb library slots (S8).
+edm_status launch_weights(uint2* tables, int64_t T_lib, const int64_t offE[ECAP + 2], unsigned maskS, int Lk, int tau,
+                          int hrz, const int* slotE, int nb, cudaStream_t cs) {
+    WeightParams WP{};
+    WP.tables = tables; WP.T_lib = T_lib; WP.nlib = nb; WP.slotE = slotE;
+    memcpy(WP.offE, offE, sizeof(WP.offE));
+    int acc = 0;
+    for (int Ev = 1; Ev <= ECAP + 1; ++Ev) {
+        WP.rowStart[Ev] = acc;
+        if (Ev <= ECAP && ((maskS >> Ev) & 1u)) acc += (int)std::max<int64_t>(n_rows(Lk, Ev, tau, hrz), 0);
+    }
+    WP.rowStart[0] = 0;
+    const int64_t nthr = (int64_t)acc * nb;
+    if (nthr == 0) return EDM_OK;
+    PROF_LAUNCH(EDM_PROF_CCM_KNN, cs, weights_kernel<<<(unsigned)((nthr + 255) / 256), 256, 0, cs>>>(WP));
+    LAUNCH_CHECK("weights_kernel");
+    return EDM_OK;
+}
+
+// Convergence-test library blocks (reading R16): for every size l and sample r, tables over the
+// library set of (l, r) (knn_kernel<CMASK>), weights, one lookup pass writing the sample's rho,
+// then the mean over the R samples. E with l - exclude_self < E+1 have no table: rho = NaN.
+edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP + 2], int64_t T_lib, unsigned maskS,
+                       int Etop, int tau, int Tp, edm_e_mode mode, int exclude_self, int nlib, int ntiles, int Np,
+                       bool use_smem, size_t lk_smem, float* rho, void* conv_base, const ConvArgs& cv, cudaStream_t cs) {
+    const int N = ds.N, L = ds.L, R = cv.R, S = cv.nsizes, ncand = L - Tp;
+    ConvWs C = conv_ws(conv_base, N, L, S, R);
+    CUDA_TRY(cudaMemcpyAsync(C.perms, cv.perms, sizeof(int) * (size_t)R * L, cudaMemcpyHostToDevice, cs));
+    CUDA_TRY(cudaMemcpyAsync(C.sizes, cv.sizes, sizeof(int) * (size_t)S, cudaMemcpyHostToDevice, cs));
+    const size_t sub_smem = (size_t)ncand * sizeof(unsigned);
+    if (sub_smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(subset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem));
+    PROF_LAUNCH(EDM_PROF_PREP, cs,
+                subset_kernel<<<S * R, 64, sub_smem, cs>>>(C.perms, L, ncand, tau, maskS, C.sizes, R, C.allow, C.allow_ld,
+                                                           C.clist, L, C.ncl));
+    LAUNCH_CHECK("subset_kernel");
+    for (int r0 = 0; r0 < nlib; r0 += CCM_B) {
+        const int nb = std::min(CCM_B, nlib - r0);
+        const int* slotE = (mode == EDM_E_LIBRARY) ? W.slotE + r0 : nullptr;
+        for (int q = 0; q < S; ++q) {
+            const int Eok = std::min(ECAP, cv.sizes[q] - (exclude_self ? 1 : 0) - 1);
+            const unsigned maskq = Eok >= 1 ? maskS & ((2u << Eok) - 2u) : 0u;
+            const int Etopq = maskq ? 31 - __builtin_clz(maskq) : 0;
+            for (int r = 0; r < R; ++r) {
+                const int64_t qr = (int64_t)q * R + r;
+                if (maskq) {
+                    KnnParams P{};
+                    P.X = W.Xs; P.ldx = L; P.slot_series = W.slot_series + r0;
+                    P.L = L; P.tau = tau; P.Tp = Tp; P.store_shift = 0; P.excl = exclude_self ? 1 : 0;
+                    P.maskS = maskq; P.Etop = Etopq; P.slotE = slotE;
+                    P.tables = W.tables; P.T_lib = T_lib;
+                    memcpy(P.offE, offE, sizeof(P.offE));
+                    P.allow = C.allow + qr * C.allow_ld; P.clist = C.clist + qr * L; P.ncl = C.ncl + qr;
+                    edm_status st = launch_knn<MODE_CCM>(P, ncand, nb, cs);
+                    if (st != EDM_OK) return st;
+                    st = launch_weights(W.tables, T_lib, offE, maskq, L, tau, Tp, slotE, nb, cs);
+                    if (st != EDM_OK) return st;
+                }
+                LookupParams Q{};
+                Q.Yp = W.Yp; Q.Np = Np; Q.colmap = W.colmap;
+                Q.tileE = (mode == EDM_E_TARGET) ? W.tileE : nullptr;
+                Q.slotE = W.slotE + r0; Q.slotRow = W.slot_row + r0;
+                Q.tables = W.tables; Q.T_lib = T_lib;
+                memcpy(Q.offE, offE, sizeof(Q.offE));
+                Q.stats = W.stats; Q.cflag = W.cflag;
+                Q.Lt = L; Q.Lk = L; Q.hrz = Tp; Q.gshift = Tp; Q.oshift = Tp;
+                Q.tau = tau; Q.B = nb; Q.N = N; Q.Eok = Eok;
+                if (cv.rho_samples) {
+                    Q.rho = cv.rho_samples; Q.rstride = (int64_t)S * R * N; Q.roff = qr * N; Q.rbase = 0;
+                } else {
+                    Q.rho = C.samples; Q.rstride = (int64_t)R * N; Q.roff = (int64_t)r * N; Q.rbase = r0;
+                }
+                if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+                else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+                LAUNCH_CHECK("lookup_kernel");
+            }
+            const float* src = cv.rho_samples ? cv.rho_samples + ((int64_t)r0 * S + q) * R * N : C.samples;
+            const int64_t s_stride = cv.rho_samples ? (int64_t)S * R * N : (int64_t)R * N;
+            const int64_t nthr = (int64_t)nb * N;
+            PROF_LAUNCH(EDM_PROF_OTHER, cs,
+                        sample_mean_kernel<<<(unsigned)((nthr + 255) / 256), 256, 0, cs>>>(
+                            src, s_stride, rho + ((int64_t)r0 * S + q) * N, (int64_t)S * N, nb, R, N));
+            LAUNCH_CHECK("sample_mean_kernel");
+        }
+    }
+    return EDM_OK;
+}
+
 // Phase 2 core, shared by edm_ccm_all_pairs (one horizon Tp: m_lo = 0, m_hi = Tp, lags [Tp,Tp])
 // and edm_ccm_lagged (lags [lag_min, lag_max]). Tables are built once per library block on the
 // points t in [(E-1)tau + m_lo, L-1-m_hi] (the kNN runs on the series shifted by m_lo, with
@@ -331,7 +464,7 @@ namespace {
 // y[label + m_lo + l] and observes y[t + l]. rho[row * nlag*N + (l - lag_min) * N + j].
 edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int m_hi, int lag_min, int lag_max,
                     edm_e_mode mode, int32_t exclude_self, int32_t lib_begin, int32_t lib_end, float* rho,
-                    void* workspace, size_t ws_bytes, size_t need, cudaStream_t cs) {
+                    void* workspace, size_t ws_bytes, size_t need, cudaStream_t cs, const ConvArgs* cv = nullptr) {
     if (need == 0 || ws_bytes < need) return fail(EDM_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
     edm_status st = check_device();
     if (st != EDM_OK) return st;
@@ -417,6 +550,8 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
     const size_t lk_smem = (use_smem ? tile_smem : 0) + lookup_ring_bytes();
     if (use_smem) CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
     else CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
+    if (cv) return conv_blocks(ds, W, offE, T_lib, maskS, Etop, tau, m_hi, mode, exclude_self, nlib, ntiles, Np,
+                               use_smem, lk_smem, rho, (char*)workspace + W.bytes, *cv, cs);
     for (int r0 = 0; r0 < nlib; r0 += CCM_B) {
         const int nb = std::min(CCM_B, nlib - r0);
         KnnParams P{};
@@ -428,21 +563,8 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
         memcpy(P.offE, offE, sizeof(offE));
         st = launch_knn<MODE_CCM>(P, Lk - m_hi, nb, cs);
         if (st != EDM_OK) return st;
-        {
-            WeightParams WP{};
-            WP.tables = W.tables; WP.T_lib = T_lib; WP.nlib = nb;
-            WP.slotE = (mode == EDM_E_LIBRARY) ? W.slotE + r0 : nullptr;
-            memcpy(WP.offE, offE, sizeof(offE));
-            int acc = 0;
-            for (int Ev = 1; Ev <= ECAP + 1; ++Ev) {
-                WP.rowStart[Ev] = acc;
-                if (Ev <= ECAP && ((maskS >> Ev) & 1u)) acc += (int)std::max<int64_t>(n_rows(Lk, Ev, tau, m_hi), 0);
-            }
-            WP.rowStart[0] = 0;
-            const int64_t nthr = (int64_t)acc * nb;
-            PROF_LAUNCH(EDM_PROF_CCM_KNN, cs, weights_kernel<<<(unsigned)((nthr + 255) / 256), 256, 0, cs>>>(WP));
-            LAUNCH_CHECK("weights_kernel");
-        }
+        st = launch_weights(W.tables, T_lib, offE, maskS, Lk, tau, m_hi, P.slotE, nb, cs);
+        if (st != EDM_OK) return st;
         for (int l = lag_min; l <= lag_max; ++l) {
             LookupParams Q{};
             Q.Yp = W.Yp; Q.Np = Np; Q.colmap = W.colmap;
@@ -455,6 +577,7 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
             Q.Lt = L; Q.Lk = Lk; Q.hrz = m_hi; Q.gshift = m_lo + l; Q.oshift = m_lo + l;
             Q.tau = tau; Q.B = nb; Q.N = N;
             Q.rho = rho; Q.rstride = (int64_t)nlag * N; Q.roff = (int64_t)(l - lag_min) * N;
+            Q.rbase = 0; Q.Eok = ECAP;
             if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
             else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
             LAUNCH_CHECK("lookup_kernel");
@@ -500,6 +623,42 @@ edm_status edm_ccm_lagged(edm_dataset ds, const int32_t* E, int32_t tau, int32_t
     const size_t need = edm_ccm_lagged_workspace_bytes(ds.N, ds.L, tau, lag_min, lag_max);
     return ccm_core(ds, E, tau, m_lo, m_hi, lag_min, lag_max, mode, exclude_self, lib_begin, lib_end, rho, workspace,
                     ws_bytes, need, (cudaStream_t)stream);
+}
+
+size_t edm_ccm_convergence_workspace_bytes(int32_t N, int32_t L, int32_t tau, int32_t Tp, int32_t n_sizes, int32_t R) {
+    if (N < 1 || L < 2 || tau < 1 || Tp < 0 || Tp >= L || n_sizes < 1 || R < 1) return 0;
+    return ccm_ws(nullptr, N, L, L, tau, Tp, 1).bytes + conv_ws(nullptr, N, L, n_sizes, R).bytes;
+}
+
+edm_status edm_ccm_convergence(edm_dataset ds, const int32_t* E, int32_t tau, int32_t Tp, edm_e_mode mode,
+                               int32_t exclude_self, const int32_t* lib_sizes, int32_t n_sizes, const int32_t* orders,
+                               int32_t R, int32_t lib_begin, int32_t lib_end, float* rho, float* rho_samples,
+                               void* workspace, size_t ws_bytes, void* stream) {
+    if (!ds.data || !E || !rho || !workspace || !lib_sizes || !orders) return fail(EDM_EINVAL, "null pointer");
+    if (ds.N < 1 || ds.L < 2 || ds.ld < ds.N || tau < 1 || Tp < 0 || Tp >= ds.L || n_sizes < 1 || R < 1 ||
+        (mode != EDM_E_TARGET && mode != EDM_E_LIBRARY))
+        return fail(EDM_EINVAL, "bad arguments N=%d L=%d ld=%lld tau=%d Tp=%d n_sizes=%d R=%d mode=%d", ds.N, ds.L,
+                    (long long)ds.ld, tau, Tp, n_sizes, R, (int)mode);
+    if (lib_begin < 0 || lib_end > ds.N || lib_begin > lib_end) return fail(EDM_EINVAL, "bad library range [%d,%d)", lib_begin, lib_end);
+    for (int q = 0; q < n_sizes; ++q)
+        if (lib_sizes[q] < 1) return fail(EDM_EINVAL, "library size %d at position %d", lib_sizes[q], q);
+    {
+        std::vector<char> seen(ds.L);
+        for (int r = 0; r < R; ++r) {
+            std::fill(seen.begin(), seen.end(), 0);
+            for (int i = 0; i < ds.L; ++i) {
+                const int v = orders[(size_t)r * ds.L + i];
+                if (v < 0 || v >= ds.L || seen[v]) return fail(EDM_EINVAL, "orders[%d] is not a permutation of 0..L-1", r);
+                seen[v] = 1;
+            }
+        }
+    }
+    if ((size_t)(ds.L - Tp) * sizeof(unsigned) > (size_t)LOOKUP_SMEM_MAX)
+        return fail(EDM_EUNSUPPORTED, "convergence test supports L - Tp <= %d", LOOKUP_SMEM_MAX / 4);
+    const size_t need = edm_ccm_convergence_workspace_bytes(ds.N, ds.L, tau, Tp, n_sizes, R);
+    ConvArgs cv{lib_sizes, n_sizes, R, orders, rho_samples};
+    return ccm_core(ds, E, tau, 0, Tp, Tp, Tp, mode, exclude_self, lib_begin, lib_end, rho, workspace, ws_bytes, need,
+                    (cudaStream_t)stream, &cv);
 }
 
 edm_status edm_causal_map_host(const float* host_data, int32_t N, int32_t L, int32_t E_max, int32_t tau, int32_t Tp,

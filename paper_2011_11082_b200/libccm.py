@@ -28,7 +28,8 @@ E_CAP = 20
 
 EXPORTS = ("edm_embed_knn", "edm_simplex_optimal_E", "edm_ccm_all_pairs", "edm_workspace_bytes",
            "edm_causal_map_host", "edm_last_error", "edm_version", "edm_profile_begin", "edm_profile_end",
-           "edm_ccm_lagged", "edm_ccm_lagged_workspace_bytes")
+           "edm_ccm_lagged", "edm_ccm_lagged_workspace_bytes", "edm_ccm_convergence",
+           "edm_ccm_convergence_workspace_bytes")
 PROF_KINDS = ("prep", "simplex_knn", "simplex_rho", "ccm_knn", "lookup", "other")
 
 
@@ -73,6 +74,11 @@ def load(path: Optional[str] = None):
     lib.edm_ccm_lagged.argtypes = [edm_dataset, vp, i32, i32, i32, i32, i32, i32, i32, vp, vp, sz, vp]
     lib.edm_ccm_lagged_workspace_bytes.restype = sz
     lib.edm_ccm_lagged_workspace_bytes.argtypes = [i32, i32, i32, i32, i32]
+    lib.edm_ccm_convergence.restype = i32
+    lib.edm_ccm_convergence.argtypes = [edm_dataset, vp, i32, i32, i32, i32, vp, i32, vp, i32, i32, i32, vp, vp, vp,
+                                        sz, vp]
+    lib.edm_ccm_convergence_workspace_bytes.restype = sz
+    lib.edm_ccm_convergence_workspace_bytes.argtypes = [i32, i32, i32, i32, i32, i32]
     lib.edm_profile_begin.restype = i32
     lib.edm_profile_begin.argtypes = []
     lib.edm_profile_end.restype = i32
@@ -212,6 +218,46 @@ def ccm_lagged(data: torch.Tensor, E: torch.Tensor, tau: int = 1, lag_min: int =
     _check(load().edm_ccm_lagged(ds, E.data_ptr(), tau, lag_min, lag_max, _mode(mode), int(exclude_self), lib_begin,
                                  lib_end, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(data.device)))
     return out
+
+
+def _workspace_for(key, nbytes: int, device) -> torch.Tensor:
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() < nbytes:
+        _ws_cache.pop(key, None)
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def ccm_convergence(data: torch.Tensor, E: torch.Tensor, lib_sizes, orders, tau: int = 1, Tp: int = 1,
+                    mode="target", exclude_self: bool = True, lib_begin: int = 0, lib_end: Optional[int] = None,
+                    samples: bool = False):
+    """CCM convergence test (edm_ccm_convergence, reading R16): rho [rows, n_sizes, N], the mean
+    over the R random library sets of each size; with samples=True also every sample
+    [rows, n_sizes, R, N]. lib_sizes: ints; orders: int32 [R, L] permutations of 0..L-1 (host)."""
+    ds = _dataset(data)
+    _require_cuda(E, torch.int32, "E")
+    E = E.contiguous()
+    if E.numel() != ds.N:
+        raise ValueError("E must have N entries")
+    sizes = np.ascontiguousarray(np.asarray(lib_sizes, dtype=np.int32).ravel())
+    orders = np.ascontiguousarray(np.atleast_2d(np.asarray(orders, dtype=np.int32)))
+    if orders.shape[1] != ds.L:
+        raise ValueError("orders must be [R, L]")
+    R = orders.shape[0]
+    lib_end = ds.N if lib_end is None else lib_end
+    rows = max(lib_end - lib_begin, 0)
+    out = torch.empty((rows, len(sizes), ds.N), dtype=torch.float32, device=data.device)
+    smp = torch.empty((rows, len(sizes), R, ds.N), dtype=torch.float32, device=data.device) if samples else None
+    nbytes = load().edm_ccm_convergence_workspace_bytes(ds.N, ds.L, tau, Tp, len(sizes), R)
+    if nbytes == 0:
+        raise EdmError(EDM_EINVAL, f"bad convergence workspace request N={ds.N} L={ds.L} sizes={len(sizes)} R={R}")
+    ws = _workspace_for(("convergence", torch.device(data.device)), nbytes, data.device)
+    _check(load().edm_ccm_convergence(ds, E.data_ptr(), tau, Tp, _mode(mode), int(exclude_self),
+                                      sizes.ctypes.data, len(sizes), orders.ctypes.data, R, lib_begin, lib_end,
+                                      out.data_ptr(), smp.data_ptr() if samples else None, ws.data_ptr(), ws.numel(),
+                                      _stream(data.device)))
+    return (out, smp) if samples else out
 
 
 def causal_map(data: torch.Tensor, E_max: int = 20, tau: int = 1, Tp: int = 1, mode="target",

@@ -69,6 +69,24 @@ def test_validation_before_device(lib):
     assert lib.edm_simplex_optimal_E(ds, 5, 1, 0, 10, fake, None, fake, 16, None) == libccm.EDM_EWORKSPACE
     assert lib.edm_ccm_all_pairs(ds, fake, 1, 1, 7, 1, 0, 10, fake, fake, 1 << 30, None) == libccm.EDM_EINVAL
     assert lib.edm_ccm_all_pairs(ds, fake, 1, 1, 0, 1, 3, 2, fake, fake, 1 << 30, None) == libccm.EDM_EINVAL
+    # convergence test: sizes must be >= 1 and every order a permutation of 0..L-1 (host arrays)
+    import numpy as np
+    sizes = np.array([10, 50], np.int32)
+    orders = np.tile(np.arange(100, dtype=np.int32), (2, 1))
+    sp, op = sizes.ctypes.data, orders.ctypes.data
+    assert lib.edm_ccm_convergence_workspace_bytes(10, 100, 1, 1, 2, 2) > 0
+    assert lib.edm_ccm_convergence_workspace_bytes(10, 100, 1, 1, 0, 2) == 0
+    orders[1, 3] = 4
+    assert lib.edm_ccm_convergence(ds, fake, 1, 1, 0, 1, sp, 2, op, 2, 0, 10, fake, None, fake, 1 << 40,
+                                   None) == libccm.EDM_EINVAL
+    assert b"permutation" in lib.edm_last_error()
+    orders[1, 3] = 3
+    sizes[1] = 0
+    assert lib.edm_ccm_convergence(ds, fake, 1, 1, 0, 1, sp, 2, op, 2, 0, 10, fake, None, fake, 1 << 40,
+                                   None) == libccm.EDM_EINVAL
+    sizes[1] = 50
+    assert lib.edm_ccm_convergence(ds, fake, 1, 1, 0, 1, sp, 2, op, 2, 0, 10, fake, None, fake, 16,
+                                   None) == libccm.EDM_EWORKSPACE
 
 
 def test_product_path_does_not_touch_the_oracle():
