@@ -151,28 +151,88 @@ def load_traffic():
 
 
 # ------------------------------------------------------------------ oracle (cpu_baseline / reference arm)
-def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None, conv=None):
-    """Time the fp64 oracle, as it stands, on a bounded sample of the same workload:
-    phase 1 for n_series series and phase 2 for n_lib library rows x all N targets.
-    Returns (pairs/s extrapolated to the whole workload, seconds, cores, description)."""
+ORACLE_RATE = 1.0e9  # oracle work units (fp64 pair-dimension updates + lookup terms) per core-second,
+                     # calibrated on the c3 cpu_baseline (phase 1 1.26e9, phase 2 0.91e9 per core-s)
+
+
+def _series_work(L, tau, emax):
+    """Phase-1 oracle work of one series: sum over E of queries x candidates x E (C2-C4)."""
+    llib = (L + 1) // 2
+    ltgt = L - llib
+    return float(sum(max(ltgt - 1 - (e - 1) * tau, 0) * max(llib - 1 - (e - 1) * tau, 0) * e
+                     for e in range(1, emax + 1)))
+
+
+def _row_work(L, tau, Tp, E, mode, i=0):
+    """Phase-2 oracle work of one library row: one table per distinct E (n_E^2 E) + N lookups."""
+    n = lambda e: float(max(L - (e - 1) * int(tau) - Tp, 0))
+    if mode == "target":
+        tables = sum(n(e) * n(e) * e for e in np.unique(E))
+        lookups = float(np.sum([n(e) * (e + 1) for e in E]))
+    else:
+        e = int(E[i])
+        tables, lookups = n(e) * n(e) * e, len(E) * n(e) * (e + 1)
+    return float(tables + lookups)
+
+
+def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None, conv=None, budget_s=12.0):
+    """Time the fp64 oracle, as it stands, on a bounded sample of the same workload: phase 1 on
+    n_series series and phase 2 on n_lib library rows x all N targets, each sized from the work
+    model above to take about budget_s seconds on the host cores. When a single series / row is
+    already over budget (long series) the sample shrinks further -- phase 1 to E = 1..E_s, phase 2
+    to the targets of one E -- and its time is scaled by the work-model ratio (stated in the
+    description). Returns (cross maps/s extrapolated to the whole workload, seconds, cores, desc)."""
     from oracle import oracle as O
     L, N = data.shape
     cores = O.nthreads_default()
+    mcode = 0 if mode == "target" else 1
+    notes = []
+    # ---- phase 1
+    w1 = _series_work(L, tau, 20)
     t0 = time.perf_counter()
-    O.simplex_all(data, 20, tau, 0, n_series, cores)
-    t1 = time.perf_counter()
-    if lags:
-        O.ccm_lagged_rows(data, E, tau, lags[0], lags[1], 0 if mode == "target" else 1, True, 0, n_lib, cores)
-    elif conv:
-        O.ccm_convergence_rows(data, E, conv[0], conv[1], tau, Tp, 0 if mode == "target" else 1, True, 0, n_lib,
-                               nthreads=cores)
+    if w1 / ORACLE_RATE <= budget_s:
+        ns = int(min(n_series, N, max(1, budget_s * cores * ORACLE_RATE / w1)))
+        O.simplex_all(data, 20, tau, 0, ns, cores)
+        t1 = time.perf_counter()
+        full1 = (t1 - t0) * N / ns
+        notes.append(f"phase 1 on {ns} series ({t1 - t0:.1f} s)")
     else:
-        O.ccm_rows(data, E, tau, Tp, 0 if mode == "target" else 1, True, 0, n_lib, False, cores)
-    t2 = time.perf_counter()
-    # whole-workload time estimate = phase-1 time x N/n_series + phase-2 time x N/n_lib
-    full = (t1 - t0) * N / n_series + (t2 - t1) * N / n_lib
-    desc = (f"oracle phase 1 on {n_series} series ({t1 - t0:.1f} s) + phase 2 on {n_lib} library rows x {N} "
-            f"targets ({t2 - t1:.1f} s), {cores} threads; value = N^2 / (extrapolated full-map time {full:.0f} s)")
+        es = max([e for e in range(1, 21) if _series_work(L, tau, e) / ORACLE_RATE <= budget_s] or [1])
+        ns = min(cores, N)
+        O.simplex_all(data, es, tau, 0, ns, cores)
+        t1 = time.perf_counter()
+        scale = w1 / _series_work(L, tau, es)
+        full1 = (t1 - t0) * scale * N / ns
+        notes.append(f"phase 1 on {ns} series at E=1..{es} ({t1 - t0:.1f} s, x{scale:.1f} by work model to E=1..20)")
+    # ---- phase 2
+    wrow = np.mean([_row_work(L, tau, Tp, E, mode, i) for i in range(min(N, 64))])
+    if lags or conv or wrow / ORACLE_RATE <= budget_s:
+        nl = int(min(n_lib, N, max(1, budget_s * cores * ORACLE_RATE / wrow))) if not (lags or conv) else n_lib
+        if lags:
+            O.ccm_lagged_rows(data, E, tau, lags[0], lags[1], mcode, True, 0, nl, cores)
+        elif conv:
+            O.ccm_convergence_rows(data, E, conv[0], conv[1], tau, Tp, mcode, True, 0, nl, nthreads=cores)
+        else:
+            O.ccm_rows(data, E, tau, Tp, mcode, True, 0, nl, False, cores)
+        t2 = time.perf_counter()
+        full2 = (t2 - t1) * N / nl
+        notes.append(f"phase 2 on {nl} library rows x {N} targets ({t2 - t1:.1f} s)")
+    else:
+        # one E only: the libraries and targets whose E is the most common value
+        e0 = int(np.bincount(E).argmax())
+        cols = np.flatnonzero(E == e0)
+        nt = int(max(1, min(len(cols), budget_s * ORACLE_RATE / (L * (e0 + 1)) / 4)))
+        sub = np.ascontiguousarray(data[:, cols[:max(nt, min(cores, len(cols)))]])
+        nl = min(cores, sub.shape[1])
+        Esub = np.full(sub.shape[1], e0, np.int32)
+        O.ccm_rows(sub, Esub, tau, Tp, mcode, True, 0, nl, False, cores)
+        t2 = time.perf_counter()
+        scale = wrow / _row_work(L, tau, Tp, Esub, mode, 0)
+        full2 = (t2 - t1) * scale * N / nl
+        notes.append(f"phase 2 on {nl} library rows x {sub.shape[1]} targets at E={e0} ({t2 - t1:.1f} s, "
+                     f"x{scale:.1f} by work model to all {N} targets and their E)")
+    full = full1 + full2
+    desc = (", ".join(notes) + f", {cores} threads; value = cross maps / (extrapolated full-map time {full:.0f} s)")
     nlag = (lags[1] - lags[0] + 1) if lags else (len(conv[0]) * len(conv[1]) if conv else 1)
     return N * N * nlag / full, t2 - t0, cores, desc
 

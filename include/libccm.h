@@ -143,8 +143,9 @@ size_t edm_ccm_lagged_workspace_bytes(int32_t N, int32_t L, int32_t tau, int32_t
  *   rho_samples : device float[(lib_end - lib_begin) * n_sizes * R * N] or NULL; entry
  *                 (((i - lib_begin) * n_sizes + q) * R + r) * N + j = sample r.
  *   workspace   : device scratch of at least edm_ccm_convergence_workspace_bytes.
- * Errors as edm_ccm_all_pairs; EUNSUPPORTED if L - Tp > 58,112 (the set bitmap is staged in
- * shared memory). Work: n_sizes * R table builds and lookup passes per library block. */
+ * Errors as edm_ccm_all_pairs; EUNSUPPORTED if the series (L + 19 tau + 32 floats plus the
+ * per-warp lists) or the set bitmap (L - Tp words) exceed shared memory (L up to about 52,000 at
+ * tau = 1). Work: n_sizes * R table builds and lookup passes per library block. */
 edm_status edm_ccm_convergence(edm_dataset ds, const int32_t *E, int32_t tau, int32_t Tp, edm_e_mode mode,
                                int32_t exclude_self, const int32_t *lib_sizes, int32_t n_sizes,
                                const int32_t *orders, int32_t R, int32_t lib_begin, int32_t lib_end, float *rho,

@@ -139,7 +139,15 @@ struct KnnParams {
     const unsigned* allow;
     const int* clist;
     const int* ncl;
+    // long series (knn_kernel<..., KNN_GSER>): slot b's series at Xpad + b * ldpad, padded with
+    // 1e30 on both sides (pad_series_kernel), read through L1 instead of shared memory
+    const float* Xpad;
+    int64_t ldpad;
 };
+
+// knn_kernel series variants: shared-memory copy, shared-memory copy + library-set mask
+// (convergence test), padded global copy (long series: keeps 5 CTAs per SM resident)
+enum { KNN_SMEM = 0, KNN_CMASK = 1, KNN_GSER = 2 };
 
 struct KnnOffsets {
     int64_t offS[ECAP + 2];
@@ -186,6 +194,9 @@ constexpr int LIST_ENTRIES = loff(ECAP);  // 230
 #ifndef CCM_KNN_UMAX
 #define CCM_KNN_UMAX 96
 #endif
+#ifndef CCM_KNN_FAST1
+#define CCM_KNN_FAST1 1
+#endif
 constexpr int KNN_UMAX = CCM_KNN_UMAX;  // candidates of the union pre-pass (up to 3 pseudo-chunks)
 struct KnnWarpSmem {
     double D[LIST_ENTRIES];
@@ -205,6 +216,21 @@ __host__ __device__ constexpr size_t knn_warp_bytes(int L) {
 }
 constexpr size_t knn_smem_bytes(int L, int tau) {
     return (size_t)KNN_WARPS * knn_warp_bytes(L) + (size_t)(knn_padl(tau) + L + KNN_PADR) * sizeof(float);
+}
+constexpr size_t knn_smem_bytes_gser(int L) { return (size_t)KNN_WARPS * knn_warp_bytes(L); }
+__host__ __device__ constexpr int64_t knn_ldpad(int L, int tau) { return ((int64_t)knn_padl(tau) + L + KNN_PADR + 3) / 4 * 4; }
+
+// Padded global copies for KNN_GSER: out[b * ldpad + padl + t] = X[row_b * ldx + t] for
+// t in [0, L), 1e30 elsewhere (row_b = slot_series[b] or b).
+__global__ void pad_series_kernel(const float* __restrict__ X, int64_t ldx, const int* __restrict__ slot_series,
+                                  int L, int padl, int64_t ldpad, int nslots, float* __restrict__ out) {
+    const int b = blockIdx.y;
+    if (b >= nslots) return;
+    const int row = slot_series ? slot_series[b] : b;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ldpad; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = i - padl;
+        out[(int64_t)b * ldpad + i] = (t >= 0 && t < L) ? X[(int64_t)row * ldx + t] : 1e30f;
+    }
 }
 
 // Merge the lanes flagged in `bal` (candidates that passed list e's prefilter; distance `cand`
@@ -240,6 +266,22 @@ __device__ __forceinline__ double list_merge(KnnWarpSmem& W, int e, unsigned bal
         } while (b);
         if (!bal) return LD[k - 1];
     }
+#if CCM_KNN_FAST1
+    if ((bal & (bal - 1u)) == 0u) {
+        // one candidate: its insertion point is the number of list keys below it; the list
+        // entries from there on move down one slot (the last one drops out)
+        const int j = __ffs(bal) - 1;
+        const double Dj = __shfl_sync(FULL, cand, j);
+        const int sj = __shfl_sync(FULL, sc, j);
+        const bool before = isList && (myD < Dj || (myD == Dj && myS < sj));
+        const int pl = __popc(__ballot_sync(FULL, before));
+        __syncwarp();
+        if (isList && !before && lane + 1 < k) { LD[lane + 1] = myD; LS[lane + 1] = myS; }
+        if (lane == j) { LD[pl] = cand; LS[pl] = sc; }
+        __syncwarp();
+        return LD[k - 1];
+    }
+#endif
     const bool isCand = (bal >> lane) & 1u;
     int nl = lane;  // rank of my list entry
     int nc = 0;     // rank of my candidate
@@ -477,11 +519,13 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
     }
 }
 
-// grid = (ceil(nq / KNN_QPB), slots); block = KNN_WARPS * 32; dynamic smem = knn_smem_bytes.
+// grid = (ceil(nq / KNN_QPB), slots); block = KNN_WARPS * 32; dynamic smem = knn_smem_bytes
+// (KNN_SMEM / KNN_CMASK) or knn_smem_bytes_gser (KNN_GSER).
 // Warp w of CTA x handles the contiguous queries [x*QPB + w*QPW, +QPW) (so that each query
 // can seed its bounds from the previous one).
-template <int MODE, bool TAU1, bool FULLMASK, bool CMASK>
+template <int MODE, bool TAU1, bool FULLMASK, int VAR>
 __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnParams P) {
+    constexpr bool CMASK = VAR == KNN_CMASK, GSER = VAR == KNN_GSER;
     extern __shared__ __align__(16) unsigned char knn_smem[];
 
     const int b = blockIdx.y;
@@ -491,12 +535,19 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnPa
     const int nx = padl + P.L + KNN_PADR;
     // the library series in shared memory, fp32 (the inputs are fp32: widening to fp64 where the
     // exact distances are formed is lossless), padded with 1e30 ((q - 1e30)^2 = +inf in fp32)
-    float* xf_pad = reinterpret_cast<float*>(knn_smem + (size_t)KNN_WARPS * knn_warp_bytes(P.L));
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
-        const int t = i - padl;
-        xf_pad[i] = (t >= 0 && t < P.L) ? xg[t] : 1e30f;
+    const float* xf_pad;
+    if (GSER) {
+        xf_pad = P.Xpad + (int64_t)b * P.ldpad;
+        (void)xg; (void)nx;
+    } else {
+        float* xs = reinterpret_cast<float*>(knn_smem + (size_t)KNN_WARPS * knn_warp_bytes(P.L));
+        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+            const int t = i - padl;
+            xs[i] = (t >= 0 && t < P.L) ? xg[t] : 1e30f;
+        }
+        __syncthreads();
+        xf_pad = xs;
     }
-    __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned char* wbase = knn_smem + (size_t)warp * knn_warp_bytes(P.L);
     KnnWarpSmem& W = *reinterpret_cast<KnnWarpSmem*>(wbase);

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -109,6 +110,7 @@ struct SimplexWs {
     float* Xs;      // [SB][L]
     double* pred;   // [SB][ECAP][LQ]
     double* rho;    // [SB][E_max]
+    float* Xpad;    // [SB][knn_ldpad(L, tau)] padded copies (long series)
     double* sd2;    // [SB][S_slot] sorted lists (squared distances)
     int* ss;        // [SB][S_slot] sorted lists (library indices)
     int64_t S_slot;
@@ -117,7 +119,7 @@ struct SimplexWs {
 };
 
 // Lists of every (E, target point): entries per slot = sum_E (E+1) * LQ.
-SimplexWs simplex_ws(void* base, int N, int L, int E_max) {
+SimplexWs simplex_ws(void* base, int N, int L, int E_max, int tau) {
     SimplexWs w{};
     const int SB = std::min(N, SIMPLEX_SLOTS);
     const int LQ = std::max(L / 2, 1);
@@ -133,6 +135,7 @@ SimplexWs simplex_ws(void* base, int N, int L, int E_max) {
     w.Xs = (float*)(b + off);   off += align_up((size_t)SB * L * sizeof(float));
     w.pred = (double*)(b + off); off += align_up((size_t)SB * ECAP * LQ * sizeof(double));
     w.rho = (double*)(b + off);  off += align_up((size_t)SB * std::max(E_max, 1) * sizeof(double));
+    w.Xpad = (float*)(b + off);  off += align_up((size_t)SB * knn_ldpad(L, tau) * sizeof(float));
     w.sd2 = (double*)(b + off);  off += align_up((size_t)SB * acc * sizeof(double));
     w.ss = (int*)(b + off);      off += align_up((size_t)SB * acc * sizeof(int));
     w.bytes = off;
@@ -151,6 +154,7 @@ struct CcmWs {
     int* slot_row;      // [N]
     int* slotE;         // [N]
     uint2* tables;      // [CCM_B][T_lib]
+    float* Xpad;        // [CCM_B][knn_ldpad(Lk, tau)] padded library series (long series)
     int64_t Npm, T_lib;
     size_t bytes;
 };
@@ -175,6 +179,7 @@ CcmWs ccm_ws(void* base, int N, int L, int Lk, int tau, int hrz, int nlag) {
     w.slot_row = (int*)take((size_t)N * sizeof(int));
     w.slotE = (int*)take((size_t)N * sizeof(int));
     w.tables = (uint2*)take((size_t)CCM_B * w.T_lib * sizeof(uint2));
+    w.Xpad = (float*)take((size_t)CCM_B * knn_ldpad(Lk, tau) * sizeof(float));
     w.bytes = off;
     return w;
 }
@@ -214,36 +219,58 @@ ConvWs conv_ws(void* base, int N, int L, int nsizes, int R) {
     return w;
 }
 
-template <int MODE, bool TAU1, bool FULL, bool CMASK>
+template <int MODE, bool TAU1, bool FULL, int VAR>
 edm_status launch_knn_t(const KnnParams& P, dim3 grid, size_t smem, cudaStream_t st) {
     if (smem > 48 * 1024)
-        CUDA_TRY(cudaFuncSetAttribute(knn_kernel<MODE, TAU1, FULL, CMASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_TRY(cudaFuncSetAttribute(knn_kernel<MODE, TAU1, FULL, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
     PROF_LAUNCH(MODE == MODE_CCM ? EDM_PROF_CCM_KNN : MODE == MODE_SIMPLEX ? EDM_PROF_SIMPLEX_KNN : EDM_PROF_OTHER, st,
-                knn_kernel<MODE, TAU1, FULL, CMASK><<<grid, KNN_WARPS * 32, smem, st>>>(P));
+                knn_kernel<MODE, TAU1, FULL, VAR><<<grid, KNN_WARPS * 32, smem, st>>>(P));
     LAUNCH_CHECK("knn_kernel");
     return EDM_OK;
 }
 
-template <int MODE, bool CMASK>
+template <int MODE, int VAR>
 edm_status launch_knn_m(const KnnParams& P, dim3 grid, size_t smem, bool full, cudaStream_t st) {
     if (P.tau == 1)
-        return full ? launch_knn_t<MODE, true, true, CMASK>(P, grid, smem, st) : launch_knn_t<MODE, true, false, CMASK>(P, grid, smem, st);
-    return full ? launch_knn_t<MODE, false, true, CMASK>(P, grid, smem, st) : launch_knn_t<MODE, false, false, CMASK>(P, grid, smem, st);
+        return full ? launch_knn_t<MODE, true, true, VAR>(P, grid, smem, st) : launch_knn_t<MODE, true, false, VAR>(P, grid, smem, st);
+    return full ? launch_knn_t<MODE, false, true, VAR>(P, grid, smem, st) : launch_knn_t<MODE, false, false, VAR>(P, grid, smem, st);
 }
 
 // Picks the specialisation: tau == 1 (constant-offset shared loads), whether every E in
-// 1..Etop is selected (no per-E membership test) and (phase 2) whether a library-set mask
-// restricts the candidates (convergence test).
+// 1..Etop is selected (no per-E membership test), and the series variant: library-set mask
+// (phase 2 convergence test, P.allow), padded global series (P.Xpad, long series), else the
+// shared-memory copy.
 template <int MODE>
 edm_status launch_knn(const KnnParams& P, int nq, int slots, cudaStream_t st) {
     dim3 grid((nq + KNN_QPB - 1) / KNN_QPB, slots);
-    const size_t smem = knn_smem_bytes(P.L, P.tau);
     const bool full = !P.slotE && P.Etop >= 1 && P.maskS == ((2u << P.Etop) - 2u);
     if constexpr (MODE == MODE_CCM) {
-        if (P.allow) return launch_knn_m<MODE, true>(P, grid, smem, full, st);
+        if (P.allow) return launch_knn_m<MODE, KNN_CMASK>(P, grid, knn_smem_bytes(P.L, P.tau), full, st);
     }
-    return launch_knn_m<MODE, false>(P, grid, smem, full, st);
+    if constexpr (MODE != MODE_EMBED) {
+        if (P.Xpad) return launch_knn_m<MODE, KNN_GSER>(P, grid, knn_smem_bytes_gser(P.L), full, st);
+    }
+    return launch_knn_m<MODE, KNN_SMEM>(P, grid, knn_smem_bytes(P.L, P.tau), full, st);
+}
+
+// Long series: a shared-memory copy of the series would leave fewer than KNN_MIN_CTAS CTAs per
+// SM, so the kNN reads a padded global copy through L1 instead (CCM_KNN_SERIES=smem|global
+// overrides, for measurements).
+bool knn_use_gser(int L, int tau) {
+    const char* env = getenv("CCM_KNN_SERIES");
+    if (env && !strcmp(env, "smem")) return knn_smem_bytes(L, tau) > (size_t)227 * 1024;  // unless it cannot fit
+    if (env && !strcmp(env, "global")) return true;
+    return (size_t)KNN_MIN_CTAS * (knn_smem_bytes(L, tau) + 1024) > (size_t)228 * 1024;
+}
+
+edm_status pad_series(const float* X, int64_t ldx, const int* slot_series, int L, int tau, int nslots, float* out,
+                      cudaStream_t cs) {
+    const int64_t ld = knn_ldpad(L, tau);
+    dim3 grid((unsigned)std::min<int64_t>((ld + 255) / 256, 64), nslots);
+    PROF_LAUNCH(EDM_PROF_PREP, cs, pad_series_kernel<<<grid, 256, 0, cs>>>(X, ldx, slot_series, L, knn_padl(tau), ld, nslots, out));
+    LAUNCH_CHECK("pad_series_kernel");
+    return EDM_OK;
 }
 
 }  // namespace
@@ -283,7 +310,7 @@ const char* edm_version(void) { return "libccm 0.1 sm_100a (fp64 exact kNN, fp32
 
 size_t edm_workspace_bytes(int32_t which, int32_t N, int32_t L, int32_t E_max, int32_t tau, int32_t Tp) {
     if (N < 1 || L < 2 || E_max < 1 || E_max > ECAP || tau < 1 || Tp < 0) return 0;
-    if (which == 0) return simplex_ws(nullptr, N, L, E_max).bytes;
+    if (which == 0) return simplex_ws(nullptr, N, L, E_max, tau).bytes;
     if (which == 1) return ccm_ws(nullptr, N, L, L, tau, Tp, 1).bytes;
     return 0;
 }
@@ -320,7 +347,8 @@ edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int
     if (st != EDM_OK) return st;
     if (s_begin == s_end) return EDM_OK;
     cudaStream_t cs = (cudaStream_t)stream;
-    SimplexWs W = simplex_ws(workspace, ds.N, ds.L, E_max);
+    SimplexWs W = simplex_ws(workspace, ds.N, ds.L, E_max, tau);
+    const bool gser = knn_use_gser(ds.L, tau);
     const int L = ds.L, Llib = (L + 1) / 2, Ltgt = L - Llib;
     const int LQ = std::max(L / 2, 1);
     // feasible E (C2): at least E+1 library candidates and 2 target queries
@@ -342,6 +370,11 @@ edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int
             P.maskS = mask; P.Etop = Etop;
             P.sd2 = W.sd2; P.ss = W.ss; P.S_slot = W.S_slot;
             memcpy(P.offS, W.offS, sizeof(W.offS));
+            if (gser) {
+                st = pad_series(W.Xs, L, nullptr, L, tau, nb, W.Xpad, cs);
+                if (st != EDM_OK) return st;
+                P.Xpad = W.Xpad; P.ldpad = knn_ldpad(L, tau);
+            }
             st = launch_knn<MODE_SIMPLEX>(P, std::max(Ltgt - 1, 1), nb, cs);
             if (st != EDM_OK) return st;
             KnnOffsets O;
@@ -550,6 +583,7 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
     const size_t lk_smem = (use_smem ? tile_smem : 0) + lookup_ring_bytes();
     if (use_smem) CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
     else CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
+    const bool gser = knn_use_gser(Lk, tau);
     if (cv) return conv_blocks(ds, W, offE, T_lib, maskS, Etop, tau, m_hi, mode, exclude_self, nlib, ntiles, Np,
                                use_smem, lk_smem, rho, (char*)workspace + W.bytes, *cv, cs);
     for (int r0 = 0; r0 < nlib; r0 += CCM_B) {
@@ -561,6 +595,11 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
         P.slotE = (mode == EDM_E_LIBRARY) ? W.slotE + r0 : nullptr;
         P.tables = W.tables; P.T_lib = T_lib;
         memcpy(P.offE, offE, sizeof(offE));
+        if (gser) {
+            st = pad_series(P.X, P.ldx, P.slot_series, Lk, tau, nb, W.Xpad, cs);
+            if (st != EDM_OK) return st;
+            P.Xpad = W.Xpad; P.ldpad = knn_ldpad(Lk, tau);
+        }
         st = launch_knn<MODE_CCM>(P, Lk - m_hi, nb, cs);
         if (st != EDM_OK) return st;
         st = launch_weights(W.tables, T_lib, offE, maskS, Lk, tau, m_hi, P.slotE, nb, cs);
@@ -653,8 +692,8 @@ edm_status edm_ccm_convergence(edm_dataset ds, const int32_t* E, int32_t tau, in
             }
         }
     }
-    if ((size_t)(ds.L - Tp) * sizeof(unsigned) > (size_t)LOOKUP_SMEM_MAX)
-        return fail(EDM_EUNSUPPORTED, "convergence test supports L - Tp <= %d", LOOKUP_SMEM_MAX / 4);
+    if ((size_t)(ds.L - Tp) * sizeof(unsigned) > (size_t)LOOKUP_SMEM_MAX || knn_smem_bytes(ds.L, tau) > (size_t)LOOKUP_SMEM_MAX)
+        return fail(EDM_EUNSUPPORTED, "convergence test: L=%d tau=%d exceeds the shared-memory series limit", ds.L, tau);
     const size_t need = edm_ccm_convergence_workspace_bytes(ds.N, ds.L, tau, Tp, n_sizes, R);
     ConvArgs cv{lib_sizes, n_sizes, R, orders, rho_samples};
     return ccm_core(ds, E, tau, 0, Tp, Tp, Tp, mode, exclude_self, lib_begin, lib_end, rho, workspace, ws_bytes, need,
