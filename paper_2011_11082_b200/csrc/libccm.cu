@@ -102,6 +102,14 @@ void table_layout(int L, int tau, int Tp, int64_t offE[ECAP + 2], int64_t* T_lib
 
 constexpr int SIMPLEX_SLOTS = 1024;   // series per phase-1 block
 constexpr int CCM_B = 16 * LOOKUP_WARPS;  // libraries per phase-2 block (16 per lookup warp)
+constexpr size_t CCM_TABLE_BUDGET = (size_t)24 << 30;  // table bytes of one block (long series)
+
+// Libraries per phase-2 block: CCM_B, fewer (a multiple of LOOKUP_WARPS) when the block's
+// tables would exceed CCM_TABLE_BUDGET (about L > 50,000).
+inline int ccm_block(int64_t T_lib) {
+    const int64_t fit = (int64_t)(CCM_TABLE_BUDGET / (sizeof(uint2) * (size_t)std::max<int64_t>(T_lib, 1)));
+    return (int)std::max<int64_t>(LOOKUP_WARPS, std::min<int64_t>(CCM_B, fit / LOOKUP_WARPS * LOOKUP_WARPS));
+}
 constexpr int LOOKUP_SMEM_MAX = 227 * 1024;
 
 inline int64_t np_max(int N) { return (int64_t)(N + TILE_J - 1) / TILE_J * TILE_J + (int64_t)TILE_J * ECAP; }
@@ -153,9 +161,10 @@ struct CcmWs {
     int* slot_series;   // [N]
     int* slot_row;      // [N]
     int* slotE;         // [N]
-    uint2* tables;      // [CCM_B][T_lib]
-    float* Xpad;        // [CCM_B][knn_ldpad(Lk, tau)] padded library series (long series)
+    uint2* tables;      // [B][T_lib]
+    float* Xpad;        // [B][knn_ldpad(Lk, tau)] padded library series (long series)
     int64_t Npm, T_lib;
+    int B;              // libraries per block (ccm_block)
     size_t bytes;
 };
 
@@ -178,8 +187,9 @@ CcmWs ccm_ws(void* base, int N, int L, int Lk, int tau, int hrz, int nlag) {
     w.slot_series = (int*)take((size_t)N * sizeof(int));
     w.slot_row = (int*)take((size_t)N * sizeof(int));
     w.slotE = (int*)take((size_t)N * sizeof(int));
-    w.tables = (uint2*)take((size_t)CCM_B * w.T_lib * sizeof(uint2));
-    w.Xpad = (float*)take((size_t)CCM_B * knn_ldpad(Lk, tau) * sizeof(float));
+    w.B = ccm_block(w.T_lib);
+    w.tables = (uint2*)take((size_t)w.B * w.T_lib * sizeof(uint2));
+    w.Xpad = (float*)take((size_t)w.B * knn_ldpad(Lk, tau) * sizeof(float));
     w.bytes = off;
     return w;
 }
@@ -198,11 +208,11 @@ struct ConvWs {
     unsigned* allow;   // [nsizes*R][allow_ld]
     int* clist;        // [nsizes*R][L]
     int* ncl;          // [nsizes*R]
-    float* samples;    // [CCM_B][R][N]
+    float* samples;    // [B][R][N]
     int64_t allow_ld;
     size_t bytes;
 };
-ConvWs conv_ws(void* base, int N, int L, int nsizes, int R) {
+ConvWs conv_ws(void* base, int N, int L, int nsizes, int R, int B) {
     ConvWs w{};
     size_t off = 0;
     char* b = (char*)base;
@@ -214,7 +224,7 @@ ConvWs conv_ws(void* base, int N, int L, int nsizes, int R) {
     w.allow = (unsigned*)take((size_t)nqr * w.allow_ld * sizeof(unsigned));
     w.clist = (int*)take((size_t)nqr * L * sizeof(int));
     w.ncl = (int*)take((size_t)nqr * sizeof(int));
-    w.samples = (float*)take((size_t)CCM_B * R * N * sizeof(float));
+    w.samples = (float*)take((size_t)B * R * N * sizeof(float));
     w.bytes = off;
     return w;
 }
@@ -429,7 +439,7 @@ edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP +
                        int Etop, int tau, int Tp, edm_e_mode mode, int exclude_self, int nlib, int ntiles, int Np,
                        bool use_smem, size_t lk_smem, float* rho, void* conv_base, const ConvArgs& cv, cudaStream_t cs) {
     const int N = ds.N, L = ds.L, R = cv.R, S = cv.nsizes, ncand = L - Tp;
-    ConvWs C = conv_ws(conv_base, N, L, S, R);
+    ConvWs C = conv_ws(conv_base, N, L, S, R, W.B);
     CUDA_TRY(cudaMemcpyAsync(C.perms, cv.perms, sizeof(int) * (size_t)R * L, cudaMemcpyHostToDevice, cs));
     CUDA_TRY(cudaMemcpyAsync(C.sizes, cv.sizes, sizeof(int) * (size_t)S, cudaMemcpyHostToDevice, cs));
     const size_t sub_smem = (size_t)ncand * sizeof(unsigned);
@@ -438,8 +448,8 @@ edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP +
                 subset_kernel<<<S * R, 64, sub_smem, cs>>>(C.perms, L, ncand, tau, maskS, C.sizes, R, C.allow, C.allow_ld,
                                                            C.clist, L, C.ncl));
     LAUNCH_CHECK("subset_kernel");
-    for (int r0 = 0; r0 < nlib; r0 += CCM_B) {
-        const int nb = std::min(CCM_B, nlib - r0);
+    for (int r0 = 0; r0 < nlib; r0 += W.B) {
+        const int nb = std::min(W.B, nlib - r0);
         const int* slotE = (mode == EDM_E_LIBRARY) ? W.slotE + r0 : nullptr;
         for (int q = 0; q < S; ++q) {
             const int Eok = std::min(ECAP, cv.sizes[q] - (exclude_self ? 1 : 0) - 1);
@@ -586,8 +596,8 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
     const bool gser = knn_use_gser(Lk, tau);
     if (cv) return conv_blocks(ds, W, offE, T_lib, maskS, Etop, tau, m_hi, mode, exclude_self, nlib, ntiles, Np,
                                use_smem, lk_smem, rho, (char*)workspace + W.bytes, *cv, cs);
-    for (int r0 = 0; r0 < nlib; r0 += CCM_B) {
-        const int nb = std::min(CCM_B, nlib - r0);
+    for (int r0 = 0; r0 < nlib; r0 += W.B) {
+        const int nb = std::min(W.B, nlib - r0);
         KnnParams P{};
         P.X = W.Xs + m_lo; P.ldx = L; P.slot_series = W.slot_series + r0;
         P.L = Lk; P.tau = tau; P.Tp = m_hi; P.store_shift = 0; P.excl = exclude_self ? 1 : 0;
@@ -666,7 +676,8 @@ edm_status edm_ccm_lagged(edm_dataset ds, const int32_t* E, int32_t tau, int32_t
 
 size_t edm_ccm_convergence_workspace_bytes(int32_t N, int32_t L, int32_t tau, int32_t Tp, int32_t n_sizes, int32_t R) {
     if (N < 1 || L < 2 || tau < 1 || Tp < 0 || Tp >= L || n_sizes < 1 || R < 1) return 0;
-    return ccm_ws(nullptr, N, L, L, tau, Tp, 1).bytes + conv_ws(nullptr, N, L, n_sizes, R).bytes;
+    const CcmWs w = ccm_ws(nullptr, N, L, L, tau, Tp, 1);
+    return w.bytes + conv_ws(nullptr, N, L, n_sizes, R, w.B).bytes;
 }
 
 edm_status edm_ccm_convergence(edm_dataset ds, const int32_t* E, int32_t tau, int32_t Tp, edm_e_mode mode,
