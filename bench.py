@@ -175,45 +175,51 @@ def _row_work(L, tau, Tp, E, mode, i=0):
     return float(tables + lookups)
 
 
-def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None, conv=None, budget_s=12.0):
+def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None, conv=None, budget_s=12.0, impl="oracle"):
     """Time the fp64 oracle, as it stands, on a bounded sample of the same workload: phase 1 on
     n_series series and phase 2 on n_lib library rows x all N targets, each sized from the work
     model above to take about budget_s seconds on the host cores. When a single series / row is
     already over budget (long series) the sample shrinks further -- phase 1 to E = 1..E_s, phase 2
     to the targets of one E -- and its time is scaled by the work-model ratio (stated in the
     description). Returns (cross maps/s extrapolated to the whole workload, seconds, cores, desc)."""
-    from oracle import oracle as O
+    if impl == "oracle":
+        from oracle import oracle as O
+        rate = ORACLE_RATE
+    else:  # the fast host implementation (SURVEY 8(f) f4), same interface for these calls
+        from cpu_baseline import cpu as O
+        rate = 4 * ORACLE_RATE
     L, N = data.shape
-    cores = O.nthreads_default()
+    cores = os.cpu_count() or 1
     mcode = 0 if mode == "target" else 1
     notes = []
     # ---- phase 1
     w1 = _series_work(L, tau, 20)
     t0 = time.perf_counter()
-    if w1 / ORACLE_RATE <= budget_s:
-        ns = int(min(n_series, N, max(1, budget_s * cores * ORACLE_RATE / w1)))
-        O.simplex_all(data, 20, tau, 0, ns, cores)
+    if w1 / rate <= budget_s:
+        ns = int(min(n_series, N, max(1, budget_s * cores * rate / w1)))
+        O.simplex_all(data, 20, tau, 0, ns, nthreads=cores)
         t1 = time.perf_counter()
         full1 = (t1 - t0) * N / ns
         notes.append(f"phase 1 on {ns} series ({t1 - t0:.1f} s)")
     else:
-        es = max([e for e in range(1, 21) if _series_work(L, tau, e) / ORACLE_RATE <= budget_s] or [1])
+        es = max([e for e in range(1, 21) if _series_work(L, tau, e) / rate <= budget_s] or [1])
         ns = min(cores, N)
-        O.simplex_all(data, es, tau, 0, ns, cores)
+        O.simplex_all(data, es, tau, 0, ns, nthreads=cores)
         t1 = time.perf_counter()
         scale = w1 / _series_work(L, tau, es)
         full1 = (t1 - t0) * scale * N / ns
         notes.append(f"phase 1 on {ns} series at E=1..{es} ({t1 - t0:.1f} s, x{scale:.1f} by work model to E=1..20)")
     # ---- phase 2
     wrow = np.mean([_row_work(L, tau, Tp, E, mode, i) for i in range(min(N, 64))])
-    if lags or conv or wrow / ORACLE_RATE <= budget_s:
-        nl = int(min(n_lib, N, max(1, budget_s * cores * ORACLE_RATE / wrow))) if not (lags or conv) else n_lib
+    if lags or conv or wrow / rate <= budget_s:
+        nl = int(min(n_lib, N, max(1, budget_s * cores * rate / wrow))) if not (lags or conv) else n_lib
         if lags:
             O.ccm_lagged_rows(data, E, tau, lags[0], lags[1], mcode, True, 0, nl, cores)
         elif conv:
             O.ccm_convergence_rows(data, E, conv[0], conv[1], tau, Tp, mcode, True, 0, nl, nthreads=cores)
         else:
-            O.ccm_rows(data, E, tau, Tp, mcode, True, 0, nl, False, cores)
+            O.ccm_rows(data, E, tau=tau, Tp=Tp, mode=mcode, exclude_self=True, lib_begin=0, lib_end=nl,
+                       nthreads=cores)
         t2 = time.perf_counter()
         full2 = (t2 - t1) * N / nl
         notes.append(f"phase 2 on {nl} library rows x {N} targets ({t2 - t1:.1f} s)")
@@ -221,11 +227,12 @@ def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None, conv=None,
         # one E only: the libraries and targets whose E is the most common value
         e0 = int(np.bincount(E).argmax())
         cols = np.flatnonzero(E == e0)
-        nt = int(max(1, min(len(cols), budget_s * ORACLE_RATE / (L * (e0 + 1)) / 4)))
+        nt = int(max(1, min(len(cols), budget_s * rate / (L * (e0 + 1)) / 4)))
         sub = np.ascontiguousarray(data[:, cols[:max(nt, min(cores, len(cols)))]])
         nl = min(cores, sub.shape[1])
         Esub = np.full(sub.shape[1], e0, np.int32)
-        O.ccm_rows(sub, Esub, tau, Tp, mcode, True, 0, nl, False, cores)
+        O.ccm_rows(sub, Esub, tau=tau, Tp=Tp, mode=mcode, exclude_self=True, lib_begin=0, lib_end=nl,
+                   nthreads=cores)
         t2 = time.perf_counter()
         scale = wrow / _row_work(L, tau, Tp, Esub, mode, 0)
         full2 = (t2 - t1) * scale * N / nl
@@ -513,6 +520,14 @@ def main():
         v, secs, cores, desc = oracle_sample(host, E_host, args.mode, tau, Tp, n_lib, min(N, 256), lags, conv)
         cpu = {"value": v, "unit": unit, "cores": cores, "kind": "oracle", "sample": desc}
 
+    # ---- fast host implementation (the CPU side of the paper's GPU-vs-CPU
+    # comparison; bit-identical to the oracle), same bounded-sample method
+    cpu_fast = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not lags and not conv:
+        v, secs, cores, desc = oracle_sample(host, E_host, args.mode, tau, Tp, N, N, impl="fast")
+        cpu_fast = {"value": v, "unit": unit, "cores": cores, "kind": "fast host implementation (cpu_baseline/)",
+                    "sample": desc, "gpu_speedup": value / v}
+
     if rank == 0:
         hist = np.bincount(E_host, minlength=E_max + 1)[1:].tolist()
         out = {
@@ -532,7 +547,7 @@ def main():
             "per_rank_ms_per_step": per_rank if world > 1 else None,
             "E_hist": hist, "k_bar": float((E_host + 1).mean()),
             "roofline": roofline_main, other_key: roofline_other,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+            "cpu_baseline": cpu, "cpu_fast": cpu_fast, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
         }
         print(json.dumps(out))
     dist.barrier()

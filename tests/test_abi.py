@@ -99,3 +99,5 @@ def test_product_path_does_not_touch_the_oracle():
                 assert "oracle" not in src.replace("oracle's", "").replace("the oracle", "").lower() or \
                     "import oracle" not in src and "from oracle" not in src, f
                 assert "import oracle" not in src and "from oracle" not in src and "liboracle" not in src, f
+                # nor the host comparison implementation (no CPU fallback anywhere in the product)
+                assert "cpu_baseline" not in src and "mpedm_cpu" not in src, f
