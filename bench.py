@@ -155,23 +155,28 @@ ORACLE_RATE = 1.0e9  # oracle work units (fp64 pair-dimension updates + lookup t
                      # calibrated on the c3 cpu_baseline (phase 1 1.26e9, phase 2 0.91e9 per core-s)
 
 
-def _series_work(L, tau, emax):
-    """Phase-1 oracle work of one series: sum over E of queries x candidates x E (C2-C4)."""
+def _series_work(L, tau, emax, fast=False):
+    """Phase-1 work of one series: the oracle recomputes every E (queries x candidates x E per
+    E); the fast implementation does one incremental pass plus one selection per E (2 per E)."""
     llib = (L + 1) // 2
     ltgt = L - llib
-    return float(sum(max(ltgt - 1 - (e - 1) * tau, 0) * max(llib - 1 - (e - 1) * tau, 0) * e
+    return float(sum(max(ltgt - 1 - (e - 1) * tau, 0) * max(llib - 1 - (e - 1) * tau, 0) * (2 if fast else e)
                      for e in range(1, emax + 1)))
 
 
-def _row_work(L, tau, Tp, E, mode, i=0):
-    """Phase-2 oracle work of one library row: one table per distinct E (n_E^2 E) + N lookups."""
+def _row_work(L, tau, Tp, E, mode, i=0, fast=False):
+    """Phase-2 work of one library row: tables (oracle: n_E^2 E per distinct E; fast: n^2 per
+    dimension up to the largest E plus n^2 per selected E) + N lookups of n_E (E+1) terms."""
     n = lambda e: float(max(L - (e - 1) * int(tau) - Tp, 0))
+    sel = np.unique(E) if mode == "target" else np.array([int(E[i])])
+    if fast:
+        tables = n(1) * n(1) * (int(sel.max()) + len(sel))
+    else:
+        tables = sum(n(e) * n(e) * e for e in sel)
     if mode == "target":
-        tables = sum(n(e) * n(e) * e for e in np.unique(E))
         lookups = float(np.sum([n(e) * (e + 1) for e in E]))
     else:
-        e = int(E[i])
-        tables, lookups = n(e) * n(e) * e, len(E) * n(e) * (e + 1)
+        lookups = len(E) * n(int(E[i])) * (int(E[i]) + 1)
     return float(tables + lookups)
 
 
@@ -187,13 +192,14 @@ def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None, conv=None,
         rate = ORACLE_RATE
     else:  # the fast host implementation, same interface for these calls
         from cpu_baseline import cpu as O
-        rate = 4 * ORACLE_RATE
+        rate = 1.5 * ORACLE_RATE
     L, N = data.shape
     cores = os.cpu_count() or 1
     mcode = 0 if mode == "target" else 1
     notes = []
     # ---- phase 1
-    w1 = _series_work(L, tau, 20)
+    fast = impl != "oracle"
+    w1 = _series_work(L, tau, 20, fast)
     t0 = time.perf_counter()
     if w1 / rate <= budget_s:
         ns = int(min(n_series, N, max(1, budget_s * cores * rate / w1)))
@@ -202,15 +208,15 @@ def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None, conv=None,
         full1 = (t1 - t0) * N / ns
         notes.append(f"phase 1 on {ns} series ({t1 - t0:.1f} s)")
     else:
-        es = max([e for e in range(1, 21) if _series_work(L, tau, e) / rate <= budget_s] or [1])
+        es = max([e for e in range(1, 21) if _series_work(L, tau, e, fast) / rate <= budget_s] or [1])
         ns = min(cores, N)
         O.simplex_all(data, es, tau, 0, ns, nthreads=cores)
         t1 = time.perf_counter()
-        scale = w1 / _series_work(L, tau, es)
+        scale = w1 / _series_work(L, tau, es, fast)
         full1 = (t1 - t0) * scale * N / ns
         notes.append(f"phase 1 on {ns} series at E=1..{es} ({t1 - t0:.1f} s, x{scale:.1f} by work model to E=1..20)")
     # ---- phase 2
-    wrow = np.mean([_row_work(L, tau, Tp, E, mode, i) for i in range(min(N, 64))])
+    wrow = np.mean([_row_work(L, tau, Tp, E, mode, i, fast) for i in range(min(N, 64))])
     if lags or conv or wrow / rate <= budget_s:
         nl = int(min(n_lib, N, max(1, budget_s * cores * rate / wrow))) if not (lags or conv) else n_lib
         if lags:
@@ -234,7 +240,7 @@ def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None, conv=None,
         O.ccm_rows(sub, Esub, tau=tau, Tp=Tp, mode=mcode, exclude_self=True, lib_begin=0, lib_end=nl,
                    nthreads=cores)
         t2 = time.perf_counter()
-        scale = wrow / _row_work(L, tau, Tp, Esub, mode, 0)
+        scale = wrow / _row_work(L, tau, Tp, Esub, mode, 0, fast)
         full2 = (t2 - t1) * scale * N / nl
         notes.append(f"phase 2 on {nl} library rows x {sub.shape[1]} targets at E={e0} ({t2 - t1:.1f} s, "
                      f"x{scale:.1f} by work model to all {N} targets and their E)")
