@@ -74,7 +74,8 @@ typedef struct {
  *   dist   : device float[n_E * (E+1)], Euclidean distance, fp32(sqrt(fp64 d2)).
  *   w      : device float[n_E * (E+1)] or NULL: exponential weights u=exp(-d/d1) (d1>0)
  *            or [d==0] (d1==0), floored at 1e-6, normalised per row.
- * Errors: EINVAL, ETOOSHORT (n_E - exclude_self < E+1), EUNSUPPORTED, ECUDA. */
+ * Errors: EINVAL, ETOOSHORT (n_E - exclude_self < E+1), EUNSUPPORTED (not sm_100, or the series
+ * does not fit shared memory: L + 19 tau beyond about 55,000 samples), ECUDA. */
 edm_status edm_embed_knn(const float *series, int32_t L, int32_t E, int32_t tau, int32_t Tp,
                          int32_t exclude_self, int32_t *idx, float *dist, float *w, void *stream);
 

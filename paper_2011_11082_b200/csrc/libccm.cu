@@ -333,6 +333,8 @@ edm_status edm_embed_knn(const float* series, int32_t L, int32_t E, int32_t tau,
     const int64_t n = n_rows(L, E, tau, Tp);
     if (n - (exclude_self ? 1 : 0) < E + 1)
         return fail(EDM_ETOOSHORT, "n_E=%lld points leave fewer than E+1=%d candidates", (long long)n, E + 1);
+    if (knn_smem_bytes(L, tau) > (size_t)227 * 1024)
+        return fail(EDM_EUNSUPPORTED, "edm_embed_knn stages the series in shared memory: L=%d tau=%d is too long", L, tau);
     edm_status st = check_device();
     if (st != EDM_OK) return st;
     KnnParams P{};
