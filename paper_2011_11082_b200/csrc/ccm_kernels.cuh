@@ -62,7 +62,13 @@ __global__ void colprep_kernel(const float* __restrict__ y, int64_t ld, int N, i
     mean[j] = s / L;
 }
 
-// Yp[t][p] = y[t][colmap[p]] - mean[colmap[p]] (0 for padding columns colmap[p] < 0).
+// Yp = the centred targets in tile-major order: column p (tile p/32, lane p%32) at time t is
+// Yp[yp_index(p, t, L)] = y[t][colmap[p]] - mean[colmap[p]] (0 for padding columns). Each
+// 32-target tile is one contiguous [L][32] block (staged whole into shared memory, or gathered
+// from L2 with 32-bit offsets for long series).
+__host__ __device__ __forceinline__ int64_t yp_index(int p, int t, int L) {
+    return ((int64_t)(p >> 5) * L + t) * 32 + (p & 31);
+}
 __global__ void permute_kernel(const float* __restrict__ y, int64_t ld, int L, int Np,
                                const int* __restrict__ colmap, const double* __restrict__ mean,
                                float* __restrict__ Yp) {
@@ -71,7 +77,7 @@ __global__ void permute_kernel(const float* __restrict__ y, int64_t ld, int L, i
     const int c = colmap[p];
     const double mu = c >= 0 ? mean[c] : 0.0;
     for (int t = blockIdx.y; t < L; t += gridDim.y)
-        Yp[(int64_t)t * Np + p] = c >= 0 ? (float)((double)y[(int64_t)t * ld + c] - mu) : 0.f;
+        Yp[yp_index(p, t, L)] = c >= 0 ? (float)((double)y[(int64_t)t * ld + c] - mu) : 0.f;
 }
 
 // Observed-window statistics for every E: the observation of table row r
@@ -79,7 +85,7 @@ __global__ void permute_kernel(const float* __restrict__ y, int64_t ld, int L, i
 // the same for every E). stats[(E-1)*Np + p] = (sum y, sum y^2) of the centred fp32 column
 // over it (fp64), cflag[(E-1)*Np + p] = 1 if every raw value in it is equal (NaN skill).
 // Single-horizon CCM: d = Tp, obs_end = L-1; time-delay cross map: d = m_lo + lag.
-__global__ void stats_kernel(const float* __restrict__ Yp, const float* __restrict__ y, int64_t ld,
+__global__ void stats_kernel(const float* __restrict__ Yp, int L, const float* __restrict__ y, int64_t ld,
                              const int* __restrict__ colmap, int Np, int tau, int d, int obs_end, int Emax,
                              double2* __restrict__ stats, int* __restrict__ cflag) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -94,7 +100,7 @@ __global__ void stats_kernel(const float* __restrict__ Yp, const float* __restri
         cflag[(int64_t)(e - 1) * Np + p] = 1;
     }
     for (int t = obs_end; t >= 0 && e >= 1; --t) {
-        const double v = (double)Yp[(int64_t)t * Np + p];
+        const double v = (double)Yp[yp_index(p, t, L)];
         s1 += v;
         s2 += v * v;
         if (c >= 0 && y[(int64_t)t * ld + c] != last) same = false;
@@ -888,7 +894,7 @@ __device__ __forceinline__ void lookup_dispatch(int E, const LookupParams& P, co
 constexpr size_t lookup_ring_bytes() { return (size_t)LOOKUP_WARPS * LK_STAGES * (LK_CHUNK + 8); }
 
 // grid = ntiles; block = LOOKUP_WARPS * 32. SMEM = true: the 32-column target tile
-// Yp[0..L)[tile*32 .. +32) is staged in shared memory ([L][32] fp32) once and reused by
+// tile block (yp_index: [L][32] contiguous) is staged in shared memory once and reused by
 // every library of the block (the table reuse of Alg. 2, turned into target-tile
 // reuse); SMEM = false (long series): gathers straight from L2/HBM. Tiles run in reverse
 // order so that the expensive high-E tiles (target mode) start first.
@@ -911,19 +917,15 @@ __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupPara
     }
     const float* Y;
     int64_t ys;
+    const float* src = P.Yp + yp_index(tile * TILE_J, 0, P.Lt);  // the tile's contiguous [L][32] block
     if (SMEM) {
-        const float* src = P.Yp + (int64_t)tile * TILE_J;
-        for (int i = threadIdx.x; i < P.Lt * (TILE_J / 4); i += blockDim.x) {
-            const int t = i / (TILE_J / 4), c = (i % (TILE_J / 4)) * 4;
-            *reinterpret_cast<float4*>(ytile + t * TILE_J + c) =
-                __ldg(reinterpret_cast<const float4*>(src + (int64_t)t * P.Np + c));
-        }
+        for (int i = threadIdx.x; i < P.Lt * (TILE_J / 4); i += blockDim.x)
+            reinterpret_cast<float4*>(ytile)[i] = __ldg(reinterpret_cast<const float4*>(src) + i);
         Y = ytile;
-        ys = TILE_J;
     } else {
-        Y = P.Yp + (int64_t)tile * TILE_J;
-        ys = P.Np;
+        Y = src;  // gathers from L2/HBM; byte offsets idx * 128 + lane * 4 stay 32-bit (L < 2^25)
     }
+    ys = TILE_J;
     __syncthreads();
     const int col = P.colmap[tile * TILE_J + lane];
     for (int b = warp; b < P.B; b += LOOKUP_WARPS) {

@@ -152,7 +152,7 @@ SimplexWs simplex_ws(void* base, int N, int L, int E_max, int tau) {
 
 struct CcmWs {
     float* Xs;          // [N][L] library series, series-major
-    float* Yp;          // [L][Npm] centred permuted targets
+    float* Yp;          // [Npm/32][L][32] centred permuted targets, tile-major (yp_index)
     int* colmap;        // [Npm]
     int* tileE;         // [Npm / 32]
     double* mean;       // [N]
@@ -583,7 +583,7 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
         for (int l = lag_min; l <= lag_max; ++l) {
             const int64_t so = (int64_t)(l - lag_min) * ECAP * W.Npm;
             PROF_LAUNCH(EDM_PROF_PREP, cs,
-                        stats_kernel<<<(Np + 127) / 128, 128, 0, cs>>>(W.Yp, ds.data, ds.ld, W.colmap, Np, tau, m_lo + l,
+                        stats_kernel<<<(Np + 127) / 128, 128, 0, cs>>>(W.Yp, L, ds.data, ds.ld, W.colmap, Np, tau, m_lo + l,
                                                                       L - 1 - m_hi + l, ECAP, W.stats + so, W.cflag + so));
             LAUNCH_CHECK("stats_kernel");
         }
