@@ -165,7 +165,9 @@ size_t edm_workspace_bytes(int32_t which, int32_t N, int32_t L, int32_t E_max, i
  * over all series, then phase 2 over all library rows, and copies the results back.
  *   host_optE : int32[N] or NULL;  host_rho : float[N * N] (row = library);
  *   host_rhoE : float[N * E_max] or NULL.
- * Blocking; allocates and frees its own device memory. Same errors as above. */
+ * Blocking; allocates and frees its own device memory. When host_rho is page-locked the map
+ * is computed in 8 row chunks and each chunk's rows are copied back on a second stream while
+ * the next chunk computes. Same errors as above. */
 edm_status edm_causal_map_host(const float *host_data, int32_t N, int32_t L, int32_t E_max,
                                int32_t tau, int32_t Tp, edm_e_mode mode, int32_t exclude_self,
                                int32_t *host_optE, float *host_rho, float *host_rhoE);

@@ -722,14 +722,22 @@ edm_status edm_causal_map_host(const float* host_data, int32_t N, int32_t L, int
     if (ws0 == 0 || ws1 == 0) return fail(EDM_EINVAL, "bad arguments N=%d L=%d E_max=%d tau=%d Tp=%d", N, L, E_max, tau, Tp);
     edm_status st = check_device();
     if (st != EDM_OK) return st;
-    cudaStream_t cs;
+    cudaStream_t cs, cs2;
     CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    if (cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamDestroy(cs);
+        return fail(EDM_ECUDA, "cudaStreamCreateWithFlags failed");
+    }
     float *d_data = nullptr, *d_rho = nullptr, *d_rhoE = nullptr;
     int32_t* d_E = nullptr;
     void* ws = nullptr;
+    std::vector<cudaEvent_t> evs;
     auto cleanup = [&]() {
+        cudaStreamSynchronize(cs2);
+        for (cudaEvent_t e : evs) cudaEventDestroy(e);
         cudaFree(d_data); cudaFree(d_rho); cudaFree(d_rhoE); cudaFree(d_E); cudaFree(ws);
         cudaStreamDestroy(cs);
+        cudaStreamDestroy(cs2);
     };
     auto run = [&]() -> edm_status {
         CUDA_TRY(cudaMalloc(&d_data, sizeof(float) * (size_t)N * L));
@@ -741,9 +749,27 @@ edm_status edm_causal_map_host(const float* host_data, int32_t N, int32_t L, int
         edm_dataset ds{d_data, N, L, N};
         edm_status s = edm_simplex_optimal_E(ds, E_max, tau, 0, N, d_E, d_rhoE, ws, std::max(ws0, ws1), cs);
         if (s != EDM_OK) return s;
-        s = edm_ccm_all_pairs(ds, d_E, tau, Tp, mode, exclude_self, 0, N, d_rho, ws, std::max(ws0, ws1), cs);
-        if (s != EDM_OK) return s;
-        CUDA_TRY(cudaMemcpyAsync(host_rho, d_rho, sizeof(float) * (size_t)N * N, cudaMemcpyDeviceToHost, cs));
+        // phase 2 in row chunks: with a page-locked host_rho each chunk's rows go back on a second
+        // stream while the next chunk computes (only the last chunk's copy is exposed)
+        cudaPointerAttributes pa{};
+        const bool pinned = cudaPointerGetAttributes(&pa, host_rho) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();  // a pageable pointer may leave an error behind on older drivers
+        const int nchunk = pinned ? 8 : 1;
+        const int step = ((N + nchunk - 1) / nchunk + CCM_B - 1) / CCM_B * CCM_B;
+        for (int r0 = 0; r0 < N; r0 += step) {
+            const int r1 = std::min(N, r0 + step);
+            s = edm_ccm_all_pairs(ds, d_E, tau, Tp, mode, exclude_self, r0, r1, d_rho + (size_t)r0 * N, ws,
+                                  std::max(ws0, ws1), cs);
+            if (s != EDM_OK) return s;
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            evs.push_back(e);
+            CUDA_TRY(cudaEventRecord(e, cs));
+            CUDA_TRY(cudaStreamWaitEvent(cs2, e, 0));
+            CUDA_TRY(cudaMemcpyAsync(host_rho + (size_t)r0 * N, d_rho + (size_t)r0 * N, sizeof(float) * (size_t)(r1 - r0) * N,
+                                     cudaMemcpyDeviceToHost, cs2));
+        }
+        CUDA_TRY(cudaStreamSynchronize(cs2));
         if (host_optE) CUDA_TRY(cudaMemcpyAsync(host_optE, d_E, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, cs));
         if (host_rhoE) CUDA_TRY(cudaMemcpyAsync(host_rhoE, d_rhoE, sizeof(float) * (size_t)N * E_max, cudaMemcpyDeviceToHost, cs));
         CUDA_TRY(cudaStreamSynchronize(cs));
