@@ -512,9 +512,7 @@ def main():
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 d = host_pinned.to(dev, non_blocking=True)
-                Eg, _, full = distributed.causal_map_distributed(d, E_max, tau, Tp, args.mode, True, gather=True)
-                if rank == 0:
-                    rho_host.copy_(full)
+                distributed.causal_map_distributed_to_host(d, rho_host, E_max, tau, Tp, args.mode, True)
                 torch.cuda.synchronize()
                 el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
                 dist.all_reduce(el, op=dist.ReduceOp.MAX)
@@ -522,7 +520,7 @@ def main():
             sec = max(ts)
         e2e = {"value": pairs / sec, "unit": "pairs/s", "seconds": sec, "h2d_bytes_per_step": Bi,
                "d2h_bytes_per_step": Bo, "api": "edm_causal_map_host (C ABI, host buffers)" if world == 1 else
-               "distributed.causal_map_distributed + pinned H2D/D2H"}
+               "distributed.causal_map_distributed_to_host (pinned H2D, chunked NCCL gather + overlapped D2H)"}
 
     # ---- CPU baseline: the oracle on a bounded sample, rank 0 at N=1 only
     cpu = None

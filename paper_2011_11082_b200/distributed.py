@@ -81,6 +81,62 @@ def run(data: torch.Tensor, E_max: int, tau: int, Tp: int, mode, exclude_self: b
     return E, rows, full
 
 
+def run_to_host(data: torch.Tensor, E_max: int, tau: int, Tp: int, mode, exclude_self: bool,
+                simplex_fn: Callable, ccm_fn: Callable, rho_host: Optional[torch.Tensor], nchunk: int = 8,
+                group=None):
+    """Sharded causal map delivered to host memory on rank 0 (rho_host [N, N], page-locked for
+    overlap; None on other ranks). Phase 2 runs in nchunk row chunks per rank; after each chunk
+    the ranks gather it to rank 0 (NCCL), and rank 0 copies it to rho_host on a side stream while
+    every rank computes the next chunk. Returns E[N]."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    N = data.shape[1]
+    s0, s1 = shard(N, rank, world)
+    E = all_gather_E(simplex_fn(data, E_max, tau, s0, s1), N, group)
+    cuda = data.is_cuda
+    side = torch.cuda.Stream(device=data.device) if (cuda and rank == 0) else None
+    # chunk c of rank r: rows [b_r + c * step_r, ...) of its block [b_r, e_r)
+    blocks = [shard(N, r, world) for r in range(world)]
+    steps = [max(1, -(-(e - b) // nchunk)) for b, e in blocks]
+    per = max(steps)
+    bufs = None
+    for c in range(nchunk):
+        b, e = blocks[rank]
+        r0, r1 = min(e, b + c * steps[rank]), min(e, b + (c + 1) * steps[rank])
+        buf = torch.full((per, N), float("nan"), dtype=torch.float32, device=data.device)
+        if r1 > r0:
+            buf[: r1 - r0] = ccm_fn(data, E, tau, Tp, mode, exclude_self, r0, r1)
+        if rank == 0:
+            gl = [torch.empty_like(buf) for _ in range(world)]
+            dist.gather(buf, gl, dst=0, group=group)
+            if side is not None:
+                side.wait_stream(torch.cuda.current_stream(data.device))
+            ctx = torch.cuda.stream(side) if side is not None else _nullctx()
+            with ctx:
+                for r in range(world):
+                    rb, re = blocks[r]
+                    q0, q1 = min(re, rb + c * steps[r]), min(re, rb + (c + 1) * steps[r])
+                    if q1 > q0:
+                        rho_host[q0:q1].copy_(gl[r][: q1 - q0], non_blocking=side is not None)
+                        if side is not None:
+                            gl[r].record_stream(side)
+        else:
+            dist.gather(buf, None, dst=0, group=group)
+        bufs = buf  # keep the last local buffer alive until the collective has consumed it
+    if side is not None:
+        side.synchronize()
+    del bufs
+    return E
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 def libccm_phase_fns():
     """The production phase functions (libccm CUDA path)."""
     from . import libccm
@@ -92,6 +148,13 @@ def libccm_phase_fns():
         return libccm.ccm_all_pairs(data, E, tau, Tp, mode, excl, l0, l1)
 
     return simplex_fn, ccm_fn
+
+
+def causal_map_distributed_to_host(data: torch.Tensor, rho_host: Optional[torch.Tensor], E_max: int = 20, tau: int = 1,
+                                   Tp: int = 1, mode="target", exclude_self: bool = True, nchunk: int = 8, group=None):
+    """Production entry with the map delivered to (page-locked) host memory on rank 0."""
+    sf, cf = libccm_phase_fns()
+    return run_to_host(data, E_max, tau, Tp, mode, exclude_self, sf, cf, rho_host, nchunk, group)
 
 
 def causal_map_distributed(data: torch.Tensor, E_max: int = 20, tau: int = 1, Tp: int = 1, mode="target",

@@ -50,6 +50,21 @@ def _worker(rank, world, port, data, out_path, mode):
     dist.destroy_process_group()
 
 
+def _worker_host(rank, world, port, data, out_path, mode, nchunk):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sf, cf = _oracle_fns()
+    N = data.shape[1]
+    host = torch.full((N, N), -7.0) if rank == 0 else None
+    E = D.run_to_host(torch.from_numpy(data), 6, 1, 1, mode, True, sf, cf, host, nchunk)
+    if rank == 0:
+        np.save(out_path + "_E.npy", E.numpy())
+        np.save(out_path + "_rho.npy", host.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def test_shard_covers_everything():
     for n in (1, 7, 64, 1001):
         for w in (1, 2, 3, 8):
@@ -66,6 +81,21 @@ def test_sharded_map_equals_single_process(tmp_path, world, mode):
     data = synth.random_dataset(13, 70, 21)
     out = str(tmp_path / "res")
     mp.spawn(_worker, args=(world, _free_port(), data, out, mode), nprocs=world, join=True)
+    E = np.load(out + "_E.npy")
+    rho = np.load(out + "_rho.npy")
+    rE, _ = O.simplex_all(data, 6, 1)
+    assert np.array_equal(E, rE)
+    ref = O.ccm_rows(data, rE, 1, 1, 0 if mode == "target" else 1, True).astype(np.float32)
+    assert np.array_equal(rho.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("world,mode,nchunk", [(2, "target", 3), (3, "library", 8)])
+def test_chunked_map_to_host_equals_single_process(tmp_path, world, mode, nchunk):
+    # the chunked gather-to-host path of the end-to-end API (more chunks than rows on some ranks)
+    from oracle import oracle as O
+    data = synth.random_dataset(11, 60, 23)
+    out = str(tmp_path / "res")
+    mp.spawn(_worker_host, args=(world, _free_port(), data, out, mode, nchunk), nprocs=world, join=True)
     E = np.load(out + "_E.npy")
     rho = np.load(out + "_rho.npy")
     rE, _ = O.simplex_all(data, 6, 1)
