@@ -81,9 +81,12 @@ def run(data: torch.Tensor, E_max: int, tau: int, Tp: int, mode, exclude_self: b
     return E, rows, full
 
 
+CHUNK_ALIGN = 256  # libraries per phase-2 block of libccm (CCM_B)
+
+
 def run_to_host(data: torch.Tensor, E_max: int, tau: int, Tp: int, mode, exclude_self: bool,
-                simplex_fn: Callable, ccm_fn: Callable, rho_host: Optional[torch.Tensor], nchunk: int = 8,
-                group=None):
+                simplex_fn: Callable, ccm_fn: Callable, rho_host: Optional[torch.Tensor], nchunk: int = 4,
+                group=None, align: int = CHUNK_ALIGN):
     """Sharded causal map delivered to host memory on rank 0 (rho_host [N, N], page-locked for
     overlap; None on other ranks). Phase 2 runs in nchunk row chunks per rank; after each chunk
     the ranks gather it to rank 0 (NCCL), and rank 0 copies it to rho_host on a side stream while
@@ -96,14 +99,20 @@ def run_to_host(data: torch.Tensor, E_max: int, tau: int, Tp: int, mode, exclude
     cuda = data.is_cuda
     side = torch.cuda.Stream(device=data.device) if (cuda and rank == 0) else None
     # chunk c of rank r: rows [b_r + c * step_r, ...) of its block [b_r, e_r)
+    # (chunks are whole multiples of the kernels' 256-library block, so none runs a partial block
+    # except at the end of a rank's rows)
     blocks = [shard(N, r, world) for r in range(world)]
-    steps = [max(1, -(-(e - b) // nchunk)) for b, e in blocks]
+    def step_of(rows):
+        want = -(-rows // nchunk)                   # ceil(rows / nchunk)
+        return max(1, -(-want // align) * align)    # rounded up to a multiple of align
+    steps = [step_of(e - b) for b, e in blocks]
+    nchunk = max(-(-(e - b) // st) for (b, e), st in zip(blocks, steps))
     per = max(steps)
     bufs = None
     for c in range(nchunk):
         b, e = blocks[rank]
         r0, r1 = min(e, b + c * steps[rank]), min(e, b + (c + 1) * steps[rank])
-        buf = torch.full((per, N), float("nan"), dtype=torch.float32, device=data.device)
+        buf = torch.empty((per, N), dtype=torch.float32, device=data.device)
         if r1 > r0:
             buf[: r1 - r0] = ccm_fn(data, E, tau, Tp, mode, exclude_self, r0, r1)
         if rank == 0:
@@ -151,7 +160,7 @@ def libccm_phase_fns():
 
 
 def causal_map_distributed_to_host(data: torch.Tensor, rho_host: Optional[torch.Tensor], E_max: int = 20, tau: int = 1,
-                                   Tp: int = 1, mode="target", exclude_self: bool = True, nchunk: int = 8, group=None):
+                                   Tp: int = 1, mode="target", exclude_self: bool = True, nchunk: int = 4, group=None):
     """Production entry with the map delivered to (page-locked) host memory on rank 0."""
     sf, cf = libccm_phase_fns()
     return run_to_host(data, E_max, tau, Tp, mode, exclude_self, sf, cf, rho_host, nchunk, group)

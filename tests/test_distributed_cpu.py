@@ -57,7 +57,7 @@ def _worker_host(rank, world, port, data, out_path, mode, nchunk):
     sf, cf = _oracle_fns()
     N = data.shape[1]
     host = torch.full((N, N), -7.0) if rank == 0 else None
-    E = D.run_to_host(torch.from_numpy(data), 6, 1, 1, mode, True, sf, cf, host, nchunk)
+    E = D.run_to_host(torch.from_numpy(data), 6, 1, 1, mode, True, sf, cf, host, nchunk, align=1)
     if rank == 0:
         np.save(out_path + "_E.npy", E.numpy())
         np.save(out_path + "_rho.npy", host.numpy())
