@@ -457,8 +457,18 @@ edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP +
             const int Eok = std::min(ECAP, cv.sizes[q] - (exclude_self ? 1 : 0) - 1);
             const unsigned maskq = Eok >= 1 ? maskS & ((2u << Eok) - 2u) : 0u;
             const int Etopq = maskq ? 31 - __builtin_clz(maskq) : 0;
+            // a size covering every row set (l >= L - Tp >= n_E) gives the same library set in every
+            // sample: compute sample 0 and copy it to the others
+            const bool whole = cv.sizes[q] >= ncand;
+            float* sbase = cv.rho_samples ? cv.rho_samples + ((int64_t)r0 * S + q) * R * N : C.samples;
+            const int64_t spitch = cv.rho_samples ? (int64_t)S * R * N : (int64_t)R * N;
             for (int r = 0; r < R; ++r) {
                 const int64_t qr = (int64_t)q * R + r;
+                if (whole && r > 0) {
+                    CUDA_TRY(cudaMemcpy2DAsync(sbase + (int64_t)r * N, spitch * sizeof(float), sbase, spitch * sizeof(float),
+                                               (size_t)N * sizeof(float), nb, cudaMemcpyDeviceToDevice, cs));
+                    continue;
+                }
                 if (maskq) {
                     KnnParams P{};
                     P.X = W.Xs; P.ldx = L; P.slot_series = W.slot_series + r0;
@@ -490,12 +500,10 @@ edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP +
                 else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
                 LAUNCH_CHECK("lookup_kernel");
             }
-            const float* src = cv.rho_samples ? cv.rho_samples + ((int64_t)r0 * S + q) * R * N : C.samples;
-            const int64_t s_stride = cv.rho_samples ? (int64_t)S * R * N : (int64_t)R * N;
             const int64_t nthr = (int64_t)nb * N;
             PROF_LAUNCH(EDM_PROF_OTHER, cs,
                         sample_mean_kernel<<<(unsigned)((nthr + 255) / 256), 256, 0, cs>>>(
-                            src, s_stride, rho + ((int64_t)r0 * S + q) * N, (int64_t)S * N, nb, R, N));
+                            sbase, spitch, rho + ((int64_t)r0 * S + q) * N, (int64_t)S * N, nb, R, N));
             LAUNCH_CHECK("sample_mean_kernel");
         }
     }
