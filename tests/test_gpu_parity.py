@@ -187,6 +187,20 @@ def test_causal_map_host_end_to_end():
     assert_rho_close(rho, O.ccm_rows(data, rE, 1, 1, 0, True))
 
 
+def test_causal_map_host_pinned_chunked_equals_pageable():
+    # a page-locked rho buffer switches edm_causal_map_host to 8 row chunks whose copies overlap
+    # the next chunk's compute; the map must be byte-identical to the one-shot (pageable) path
+    data = synth.make_config("c2", N=2200, L=300)
+    N = data.shape[1]
+    E1, r1 = libccm.causal_map_host(data, 12, 1, 1)
+    pinned = torch.empty((N, N), dtype=torch.float32).pin_memory().numpy()
+    E2, r2 = libccm.causal_map_host(data, 12, 1, 1, rho_out=pinned)
+    np.testing.assert_array_equal(E1, E2)
+    assert np.array_equal(r1.view(np.uint32), r2.view(np.uint32))
+    pick = [0, 700, 2199]
+    assert_rho_close(r2[pick], np.concatenate([O.ccm_rows(data, E1, 1, 1, 0, True, p, p + 1) for p in pick]))
+
+
 def test_sugihara_direction_on_gpu():
     data = synth.sugihara_pair(1000)
     rho = libccm.ccm_all_pairs(dev(data), dev(np.array([2, 2]), torch.int32)).cpu().numpy()
