@@ -518,7 +518,7 @@ def main():
                 dist.all_reduce(el, op=dist.ReduceOp.MAX)
                 ts.append(float(el.item()))
             sec = max(ts)
-        e2e = {"value": pairs / sec, "unit": "pairs/s", "seconds": sec, "h2d_bytes_per_step": Bi,
+        e2e = {"value": pairs / sec, "unit": "pairs/s", "seconds": sec, "seconds_each": ts, "h2d_bytes_per_step": Bi,
                "d2h_bytes_per_step": Bo, "api": "edm_causal_map_host (C ABI, host buffers)" if world == 1 else
                "distributed.causal_map_distributed_to_host (pinned H2D, chunked NCCL gather + overlapped D2H)"}
 
