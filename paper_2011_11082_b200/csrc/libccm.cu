@@ -572,6 +572,26 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
     const int nlib = lib_end - lib_begin;
     std::vector<int> sser(nlib), srow(nlib), sE(nlib);
     for (int r = 0; r < nlib; ++r) { sser[r] = r; srow[r] = r; sE[r] = hE[lib_begin + r]; }
+    if (mode == EDM_E_LIBRARY) {
+        // library mode: a lookup warp handles slots w, w+16, ... of a block and its cost grows with
+        // its libraries' E, so each block's libraries are sorted by E (descending, stable) and dealt
+        // to the warps in snake order, which balances the 16 warps of every tile
+        const int B = ccm_block(T_lib);
+        for (int r0 = 0; r0 < nlib; r0 += B) {
+            const int nb = std::min(B, nlib - r0);
+            std::vector<int> ord(nb);
+            for (int i = 0; i < nb; ++i) ord[i] = r0 + i;
+            std::stable_sort(ord.begin(), ord.end(), [&](int a, int c) { return hE[lib_begin + a] > hE[lib_begin + c]; });
+            for (int p = 0; p < nb; ++p) {
+                const int m = p / LOOKUP_WARPS, j = p % LOOKUP_WARPS;
+                const bool full_round = (m + 1) * LOOKUP_WARPS <= nb;
+                const int slot = r0 + m * LOOKUP_WARPS + ((m & 1) && full_round ? LOOKUP_WARPS - 1 - j : j);
+                sser[slot] = ord[p];
+                srow[slot] = ord[p];
+                sE[slot] = hE[lib_begin + ord[p]];
+            }
+        }
+    }
     CUDA_TRY(cudaMemcpyAsync(W.colmap, colmap.data(), sizeof(int) * Np, cudaMemcpyHostToDevice, cs));
     CUDA_TRY(cudaMemcpyAsync(W.tileE, tileE.data(), sizeof(int) * ntiles, cudaMemcpyHostToDevice, cs));
     CUDA_TRY(cudaMemcpyAsync(W.slot_series, sser.data(), sizeof(int) * nlib, cudaMemcpyHostToDevice, cs));
