@@ -149,6 +149,7 @@ struct KnnParams {
     // 1e30 on both sides (pad_series_kernel), read through L1 instead of shared memory
     const float* Xpad;
     int64_t ldpad;
+    int qpw;                // queries per warp of this launch (0: KNN_QPW)
 };
 
 // knn_kernel series variants: shared-memory copy, shared-memory copy + library-set mask
@@ -525,7 +526,7 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
     }
 }
 
-// grid = (ceil(nq / KNN_QPB), slots); block = KNN_WARPS * 32; dynamic smem = knn_smem_bytes
+// grid = (ceil(nq / (KNN_WARPS * qpw)), slots); block = KNN_WARPS * 32; dynamic smem = knn_smem_bytes
 // (KNN_SMEM / KNN_CMASK) or knn_smem_bytes_gser (KNN_GSER).
 // Warp w of CTA x handles the contiguous queries [x*QPB + w*QPW, +QPW) (so that each query
 // can seed its bounds from the previous one).
@@ -582,8 +583,9 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnPa
         qaf = cbf = xf;
         nq = ncand = P.L - P.Tp;          // P_1 = [0, L-1-Tp]; per-E lower bound (E-1)tau
     }
-    const int t0 = blockIdx.x * KNN_QPB + warp * KNN_QPW;
-    const int t1 = min(nq, t0 + KNN_QPW);
+    const int qpw = P.qpw > 0 ? P.qpw : KNN_QPW;  // launch-balanced run length (<= KNN_QPW)
+    const int t0 = (blockIdx.x * KNN_WARPS + warp) * qpw;
+    const int t1 = min(nq, t0 + qpw);
     const int ncl = CMASK ? __ldg(P.ncl) : 0;
     if (t0 < t1) knn_warp<MODE, TAU1, FULLMASK, CMASK>(P, W, memb, mw, qaf, cbf, t0, t1, ncand, ncl, mask, Etop, b, lane);
 }

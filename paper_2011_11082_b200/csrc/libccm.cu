@@ -252,8 +252,13 @@ edm_status launch_knn_m(const KnnParams& P, dim3 grid, size_t smem, bool full, c
 // (phase 2 convergence test, P.allow), padded global series (P.Xpad, long series), else the
 // shared-memory copy.
 template <int MODE>
-edm_status launch_knn(const KnnParams& P, int nq, int slots, cudaStream_t st) {
-    dim3 grid((nq + KNN_QPB - 1) / KNN_QPB, slots);
+edm_status launch_knn(const KnnParams& P0, int nq, int slots, cudaStream_t st) {
+    // the fewest CTAs of KNN_QPW-query warps, then the run length that spreads the queries
+    // evenly over them (no nearly idle last CTA: 1449 queries -> 16 CTAs of 4 x 23)
+    KnnParams P = P0;
+    const int ncta = std::max(1, (nq + KNN_QPB - 1) / KNN_QPB);
+    P.qpw = std::max(1, (nq + ncta * KNN_WARPS - 1) / (ncta * KNN_WARPS));
+    dim3 grid((nq + KNN_WARPS * P.qpw - 1) / (KNN_WARPS * P.qpw), slots);
     const bool full = !P.slotE && P.Etop >= 1 && P.maskS == ((2u << P.Etop) - 2u);
     if constexpr (MODE == MODE_CCM) {
         if (P.allow) return launch_knn_m<MODE, KNN_CMASK>(P, grid, knn_smem_bytes(P.L, P.tau), full, st);
