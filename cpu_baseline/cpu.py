@@ -16,8 +16,9 @@ FLAGS = ["-O3", "-mavx2", "-fopenmp", "-std=gnu11", "-ffp-contract=off", "-fno-f
 
 def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", *FLAGS, "-o", _LIB + ".tmp", _SRC, "-lm"])
-        os.replace(_LIB + ".tmp", _LIB)
+        tmp = f"{_LIB}.tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *FLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
     return _LIB
 
 

@@ -26,8 +26,10 @@ def build(force: bool = False) -> str:
     """Compile the oracle with plain gcc: -O2 -ffp-contract=off (no FMA contraction, no
     fast-math), so each fp64 add/sub/mul is separately rounded as written."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = f"{_LIB}.tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
-                               "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm", "-lpthread"])
+                               "-fPIC", "-shared", "-o", tmp, _SRC, "-lm", "-lpthread"])
+        os.replace(tmp, _LIB)
     return _LIB
 
 

@@ -39,12 +39,13 @@ def _stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or _stale():
-        cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", LIB + ".tmp", *sources()]
+        tmp = f"{LIB}.tmp{os.getpid()}"  # per process: concurrent ranks never write the same file
+        cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", tmp, *sources()]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         os.makedirs(os.path.dirname(LIB), exist_ok=True)
         subprocess.check_call(cmd)
-        os.replace(LIB + ".tmp", LIB)
+        os.replace(tmp, LIB)  # atomic
     return LIB
 
 
