@@ -319,7 +319,9 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
         dist.init_process_group("gloo", rank=0, world_size=1)
-    build.build()
+    if rank == 0:
+        build.build()  # one compile if the in-tree library is stale; the other ranks wait for it
+    dist.barrier()
     libccm.load()
 
     cfg = synth.CONFIGS[args.config]
