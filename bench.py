@@ -118,6 +118,26 @@ def lookup_smem_bytes(E: np.ndarray, L: int, tau: int, Tp: int, mode: str) -> fl
     return float(N * per_target.sum())               # library mode: row i uses E_i for all N targets
 
 
+# Shared-memory pipe cost of one lookup row per warp (32 targets), in SM clocks: a conflict-free
+# 32-lane gather takes 1 clock, a warp-uniform 16-byte table broadcast 2 (tools/shfl_bench.cu on
+# this B200 measures 0.90 and 0.48 per clock per SM including its loop overhead,
+# profiles/r01_mio_microbench.txt); a row = k gathers + ceil(k/2) broadcasts + 1 observation read.
+GATHER_CLK, BCAST16_CLK = 1.0, 2.0
+
+
+def lookup_pipe_cycles(E: np.ndarray, L: int, tau: int, Tp: int, mode: str) -> float:
+    """SM-clock cycles of the whole map's lookup on the shared-memory pipe (model above)."""
+    E = E.astype(np.int64)
+    n = lambda e: max(L - (e - 1) * tau - Tp, 0)
+    row = lambda e: (e + 1) * GATHER_CLK + ((e + 2) // 2) * BCAST16_CLK + GATHER_CLK
+    N = len(E)
+    if mode == "target":
+        cnt = np.bincount(E, minlength=21)
+        return float(sum(-(-int(cnt[e]) // 32) * N * n(e) * row(e) for e in range(1, 21) if cnt[e]))
+    ntiles = -(-N // 32)
+    return float(sum(ntiles * n(int(e)) * row(int(e)) for e in E))
+
+
 def knn_fp64_ops(E: np.ndarray, L: int, tau: int, Tp: int, mode: str, lib_size: int | None = None) -> float:
     """Algorithmic fp64 operations of the phase-2 distance pass: for each library, every
     ordered pair (t, s != t) of P_E at every E up to the largest needed E costs one
@@ -453,6 +473,11 @@ def main():
                        "measured smem peak in MEASURED_PEAKS.json)",
         "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_s * 1e3, "launches": lk_n,
         "share_of_step": lk_ms / ms_local if ms_local else None,
+        "pipe_model": {"frac": (lookup_pipe_cycles(E_host, L, tau, Tp, args.mode) * rows_frac * nlag * args.steps /
+                                (nsm * sm_max_mhz * 1e6) / (lk_ms / 1e3)) if (lk_n and not conv) else None,
+                       "note": "ideal shared-memory-pipe time of this instruction mix (per row: k gathers x 1 clk "
+                               "+ ceil(k/2) uniform 16-B table broadcasts x 2 clk + 1 observation x 1 clk, costs from "
+                               "tools/shfl_bench.cu) / measured lookup time"},
         "hbm_view": {"bound": "hbm", "target_tile_bytes_per_launch": ntiles_bytes,
                      "achieved": ntiles_bytes / avg_launch_s / 1e9 if lk_n else None, "peak": hbm_peak,
                      "frac": (ntiles_bytes / avg_launch_s / 1e9 / hbm_peak) if lk_n else None,
