@@ -744,6 +744,7 @@ struct LookupParams {
     float* rho;             // rho[(slotRow - rbase) * rstride + roff + col]
     int64_t rstride, roff, rbase;
     int Eok;                // E > Eok: no table (convergence test, library set too small) -> NaN
+    int ntiles, nsplit;     // the last nsplit tiles run as two CTAs (library halves) each
 };
 
 // ---- per-warp table staging: TMA bulk copies (cp.async.bulk) into a 2-stage shared-memory
@@ -904,7 +905,21 @@ constexpr size_t lookup_ring_bytes() { return (size_t)LOOKUP_WARPS * LK_STAGES *
 template <bool SMEM>
 __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupParams P) {
     extern __shared__ __align__(16) unsigned char lk_smem[];
-    const int tile = gridDim.x - 1 - blockIdx.x;
+    // CTAs 0 .. ntiles-nsplit-1 take whole tiles from the last (target mode: highest E, the
+    // most expensive) down; the remaining nsplit cheapest tiles run as two CTAs each, one per
+    // half of the block's libraries, which halves the last wave's imbalance
+    int tile, b_lo = 0, b_hi = P.B;
+    {
+        const int whole = P.ntiles - P.nsplit;
+        if ((int)blockIdx.x < whole) {
+            tile = P.ntiles - 1 - blockIdx.x;
+        } else {
+            const int i = blockIdx.x - whole, half = (P.B + 1) / 2;
+            tile = P.nsplit - 1 - i / 2;
+            b_lo = (i & 1) ? half : 0;
+            b_hi = (i & 1) ? P.B : half;
+        }
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int Et = P.tileE ? P.tileE[tile] : 0;
     if (P.tileE && Et <= 0) return;
@@ -930,7 +945,7 @@ __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupPara
     ys = TILE_J;
     __syncthreads();
     const int col = P.colmap[tile * TILE_J + lane];
-    for (int b = warp; b < P.B; b += LOOKUP_WARPS) {
+    for (int b = b_lo + warp; b < b_hi; b += LOOKUP_WARPS) {
         const int E = P.tileE ? Et : P.slotE[b];
         if (E > P.Eok) {
             if (col >= 0) P.rho[((int64_t)P.slotRow[b] - P.rbase) * P.rstride + P.roff + col] = CUDART_NAN_F;

@@ -279,6 +279,20 @@ bool knn_use_gser(int L, int tau) {
     return (size_t)KNN_MIN_CTAS * (knn_smem_bytes(L, tau) + 1024) > (size_t)228 * 1024;
 }
 
+// Lookup tiles run as two half-CTAs in the last wave (CCM_LK_SPLIT=n overrides the count, 0 = off).
+int lookup_nsplit(int ntiles) {
+    const char* env = getenv("CCM_LK_SPLIT");
+    int n = 0;
+    if (env) {
+        n = atoi(env);
+    } else {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return std::max(0, std::min(n, ntiles));
+}
+
 edm_status pad_series(const float* X, int64_t ldx, const int* slot_series, int L, int tau, int nslots, float* out,
                       cudaStream_t cs) {
     const int64_t ld = knn_ldpad(L, tau);
@@ -496,13 +510,14 @@ edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP +
                 Q.stats = W.stats; Q.cflag = W.cflag;
                 Q.Lt = L; Q.Lk = L; Q.hrz = Tp; Q.gshift = Tp; Q.oshift = Tp;
                 Q.tau = tau; Q.B = nb; Q.N = N; Q.Eok = Eok;
+                Q.ntiles = ntiles; Q.nsplit = lookup_nsplit(ntiles);
                 if (cv.rho_samples) {
                     Q.rho = cv.rho_samples; Q.rstride = (int64_t)S * R * N; Q.roff = qr * N; Q.rbase = 0;
                 } else {
                     Q.rho = C.samples; Q.rstride = (int64_t)R * N; Q.roff = (int64_t)r * N; Q.rbase = r0;
                 }
-                if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
-                else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+                if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles + Q.nsplit, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+                else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles + Q.nsplit, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
                 LAUNCH_CHECK("lookup_kernel");
             }
             const int64_t nthr = (int64_t)nb * N;
@@ -662,8 +677,9 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
             Q.tau = tau; Q.B = nb; Q.N = N;
             Q.rho = rho; Q.rstride = (int64_t)nlag * N; Q.roff = (int64_t)(l - lag_min) * N;
             Q.rbase = 0; Q.Eok = ECAP;
-            if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
-            else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+            Q.ntiles = ntiles; Q.nsplit = lookup_nsplit(ntiles);
+            if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles + Q.nsplit, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+            else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles + Q.nsplit, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
             LAUNCH_CHECK("lookup_kernel");
         }
     }
