@@ -183,12 +183,12 @@ const char *edm_last_error(void);
  * EDM_PROF_KINDS, either may be NULL). Events add ~1 us of host time per launch. */
 #define EDM_PROF_KINDS 6
 enum {
-    EDM_PROF_PREP = 0,        /* transposes, target ordering, centring, window sums */
+    EDM_PROF_PREP = 0,        /* transposes, padding, target ordering, centring, window sums, library sets */
     EDM_PROF_SIMPLEX_KNN = 1, /* phase-1 distance + select + forecast */
     EDM_PROF_SIMPLEX_RHO = 2, /* phase-1 Pearson + argmax */
     EDM_PROF_CCM_KNN = 3,     /* phase-2 distance + select + weights -> tables */
     EDM_PROF_LOOKUP = 4,      /* phase-2 lookup + fused Pearson */
-    EDM_PROF_OTHER = 5        /* edm_embed_knn */
+    EDM_PROF_OTHER = 5        /* edm_embed_knn, convergence-test sample means */
 };
 edm_status edm_profile_begin(void);
 edm_status edm_profile_end(double *ms, int64_t *launches);
