@@ -744,7 +744,8 @@ struct LookupParams {
     float* rho;             // rho[(slotRow - rbase) * rstride + roff + col]
     int64_t rstride, roff, rbase;
     int Eok;                // E > Eok: no table (convergence test, library set too small) -> NaN
-    int ntiles, nsplit;     // the last nsplit tiles run as two CTAs (library halves) each
+    int ntiles, nsplit;     // the last nsplit tiles run as `parts` CTAs each (library ranges)
+    int parts;
 };
 
 // ---- per-warp table staging: TMA bulk copies (cp.async.bulk) into a 2-stage shared-memory
@@ -906,18 +907,20 @@ template <bool SMEM>
 __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupParams P) {
     extern __shared__ __align__(16) unsigned char lk_smem[];
     // CTAs 0 .. ntiles-nsplit-1 take whole tiles from the last (target mode: highest E, the
-    // most expensive) down; the remaining nsplit cheapest tiles run as two CTAs each, one per
-    // half of the block's libraries, which halves the last wave's imbalance
+    // most expensive) down; the remaining nsplit cheapest tiles run as `parts` CTAs each, one per
+    // range of the block's libraries: two in the last wave of a large map (halves its imbalance),
+    // more when there are fewer tiles than SMs (small N)
     int tile, b_lo = 0, b_hi = P.B;
     {
         const int whole = P.ntiles - P.nsplit;
         if ((int)blockIdx.x < whole) {
             tile = P.ntiles - 1 - blockIdx.x;
         } else {
-            const int i = blockIdx.x - whole, half = (P.B + 1) / 2;
-            tile = P.nsplit - 1 - i / 2;
-            b_lo = (i & 1) ? half : 0;
-            b_hi = (i & 1) ? P.B : half;
+            const int i = blockIdx.x - whole, part = i % P.parts;
+            const int per = (P.B + P.parts - 1) / P.parts;
+            tile = P.nsplit - 1 - i / P.parts;
+            b_lo = min(P.B, part * per);
+            b_hi = min(P.B, b_lo + per);
         }
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

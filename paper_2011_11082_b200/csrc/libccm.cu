@@ -279,18 +279,21 @@ bool knn_use_gser(int L, int tau) {
     return (size_t)KNN_MIN_CTAS * (knn_smem_bytes(L, tau) + 1024) > (size_t)228 * 1024;
 }
 
-// Lookup tiles run as two half-CTAs in the last wave (CCM_LK_SPLIT=n overrides the count, 0 = off).
-int lookup_nsplit(int ntiles) {
+// Lookup work split: the last nsplit tiles run as `parts` CTAs over library ranges -- one SM
+// count of tiles in halves for a large map, every tile in up to B/16 parts when there are fewer
+// tiles than two waves need (CCM_LK_SPLIT=n overrides nsplit, 0 = off).
+void lookup_split(int ntiles, int B, LookupParams& Q) {
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const char* env = getenv("CCM_LK_SPLIT");
-    int n = 0;
-    if (env) {
-        n = atoi(env);
-    } else {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return std::max(0, std::min(n, ntiles));
+    int nsplit = env ? atoi(env) : sms;
+    nsplit = std::max(0, std::min(nsplit, ntiles));
+    int parts = 2;
+    if (ntiles < 2 * sms) parts = std::max(2, std::min(std::max(B / LOOKUP_WARPS, 1), (2 * sms + ntiles - 1) / std::max(ntiles, 1)));
+    if (nsplit == 0 || B < 2) { nsplit = 0; parts = 1; }
+    Q.ntiles = ntiles;
+    Q.nsplit = nsplit;
+    Q.parts = parts;
 }
 
 edm_status pad_series(const float* X, int64_t ldx, const int* slot_series, int L, int tau, int nslots, float* out,
@@ -510,14 +513,14 @@ edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP +
                 Q.stats = W.stats; Q.cflag = W.cflag;
                 Q.Lt = L; Q.Lk = L; Q.hrz = Tp; Q.gshift = Tp; Q.oshift = Tp;
                 Q.tau = tau; Q.B = nb; Q.N = N; Q.Eok = Eok;
-                Q.ntiles = ntiles; Q.nsplit = lookup_nsplit(ntiles);
+                lookup_split(ntiles, nb, Q);
                 if (cv.rho_samples) {
                     Q.rho = cv.rho_samples; Q.rstride = (int64_t)S * R * N; Q.roff = qr * N; Q.rbase = 0;
                 } else {
                     Q.rho = C.samples; Q.rstride = (int64_t)R * N; Q.roff = (int64_t)r * N; Q.rbase = r0;
                 }
-                if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles + Q.nsplit, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
-                else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles + Q.nsplit, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+                if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+                else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
                 LAUNCH_CHECK("lookup_kernel");
             }
             const int64_t nthr = (int64_t)nb * N;
@@ -677,9 +680,9 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
             Q.tau = tau; Q.B = nb; Q.N = N;
             Q.rho = rho; Q.rstride = (int64_t)nlag * N; Q.roff = (int64_t)(l - lag_min) * N;
             Q.rbase = 0; Q.Eok = ECAP;
-            Q.ntiles = ntiles; Q.nsplit = lookup_nsplit(ntiles);
-            if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles + Q.nsplit, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
-            else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles + Q.nsplit, LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+            lookup_split(ntiles, nb, Q);
+            if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+            else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
             LAUNCH_CHECK("lookup_kernel");
         }
     }
