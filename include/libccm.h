@@ -15,8 +15,18 @@
  *  - `stream` is a cudaStream_t (NULL = legacy default stream). Arguments are validated
  *    synchronously; on EDM_OK all GPU work is enqueued on `stream` and the call returns
  *    without waiting for it (device faults surface at the caller's next synchronisation).
- *    Exception: edm_ccm_all_pairs / edm_simplex_optimal_E copy the small per-series E[]
- *    vector to the host to validate and plan (one stream synchronisation per call).
+ *    Exception: every call that takes a dataset first checks it on the device (scan_kernel)
+ *    and, for phase 2, copies the small per-series E[] vector to the host to validate and
+ *    plan -- one stream synchronisation per call (edm_embed_knn: one L-float copy).
+ *  - Input domain (reading R17): every value must be finite; a NaN or +-inf
+ *    anywhere in the dataset (phase 2: any series, since every series is a target) returns
+ *    EDM_EINVAL -- the paper's distances and Pearson rho are undefined
+ *    for them. Any finite magnitude is accepted: before the kNN sweep a series whose max |x|
+ *    lies outside [2^-40, 2^60) is rescaled by an exact power of two (distances scale
+ *    exactly, so indices are unchanged and stored distances are scaled back exactly); a
+ *    series that cannot be rescaled exactly (max |x| >= 2^60 together with values below
+ *    about 2^-66 in the same series) returns EDM_EUNSUPPORTED. No table ever holds a label
+ *    outside the series.
  *  - Indices are 0-based. Time labels: an embedded point is labelled by its
  *    latest time t, p(t) = (x[t], x[t-tau], ..., x[t-(E-1)tau]).
  *  - Undefined skill (a constant target) is a quiet NaN, never an error.
@@ -74,8 +84,9 @@ typedef struct {
  *   dist   : device float[n_E * (E+1)], Euclidean distance, fp32(sqrt(fp64 d2)).
  *   w      : device float[n_E * (E+1)] or NULL: exponential weights u=exp(-d/d1) (d1>0)
  *            or [d==0] (d1==0), floored at 1e-6, normalised per row.
- * Errors: EINVAL, ETOOSHORT (n_E - exclude_self < E+1), EUNSUPPORTED (not sm_100, or the series
- * does not fit shared memory: L + 19 tau beyond about 55,000 samples), ECUDA. */
+ * Errors: EINVAL (also a non-finite series value), ETOOSHORT (n_E - exclude_self < E+1),
+ * EUNSUPPORTED (not sm_100, or the series does not fit shared memory: L + 19 tau beyond about
+ * 55,000 samples), ECUDA. */
 edm_status edm_embed_knn(const float *series, int32_t L, int32_t E, int32_t tau, int32_t Tp,
                          int32_t exclude_self, int32_t *idx, float *dist, float *w, void *stream);
 
@@ -154,6 +165,34 @@ edm_status edm_ccm_convergence(edm_dataset ds, const int32_t *E, int32_t tau, in
 size_t edm_ccm_convergence_workspace_bytes(int32_t N, int32_t L, int32_t tau, int32_t Tp, int32_t n_sizes,
                                            int32_t R);
 
+/* Phase-2 kNN table readback (test / inspection hook for the hot path's tables, Alg. 2 line 5
+ * "kNN(ts[i], ts[i], E)", selected by partialSort): runs the SAME table
+ * build as edm_ccm_all_pairs / edm_ccm_lagged / edm_ccm_convergence (same kernels, same
+ * specialisations, same library blocks and launch configuration; weights fused into the
+ * kNN), then copies out the table of dimension Eq of every library in [lib_begin, lib_end)
+ * instead of running the lookup.
+ *   lag_min, lag_max : table geometry of edm_ccm_lagged; lag_min = lag_max = Tp >= 0 is the
+ *                      single-horizon table of edm_ccm_all_pairs. Rows are the points
+ *                      t = (Eq-1)tau + m_lo + r, r < n = L - (Eq-1)tau - m_lo - m_hi.
+ *   order, lib_size  : NULL / ignored for the full library set; else the convergence-test set
+ *                      of edm_ccm_convergence for ONE size lib_size and ONE sample (HOST
+ *                      int32[L], a permutation of 0..L-1; requires lag_min = lag_max >= 0).
+ *   Eq               : target mode: must be one of the values in E[] (else EINVAL: no table
+ *                      is built at it); library mode: only libraries i with E[i] = Eq are
+ *                      written, the rows of the others are left untouched.
+ *   idx  : device int32[(lib_end-lib_begin) * n * (Eq+1)], entry ((i-lib_begin)*n + r)*(Eq+1)+j
+ *          = label (time index, original coordinates) of the j-th neighbour of row r, sorted
+ *          by (squared distance, label); bit-exact with the oracle (lowest index on ties).
+ *   dist : device float[same] or NULL: fp32(sqrt(fp64 d2)), exactly the oracle's value.
+ *   w    : device float[same] or NULL: the weights the lookup uses (fp32 exp, within 1e-6).
+ *   workspace : >= edm_ccm_tables_workspace_bytes(N, L, tau, lag_min, lag_max).
+ * Errors as edm_ccm_all_pairs / edm_ccm_convergence. */
+edm_status edm_ccm_tables(edm_dataset ds, const int32_t *E, int32_t tau, int32_t lag_min, int32_t lag_max,
+                          edm_e_mode mode, int32_t exclude_self, int32_t lib_size, const int32_t *order,
+                          int32_t lib_begin, int32_t lib_end, int32_t Eq, int32_t *idx, float *dist, float *w,
+                          void *workspace, size_t ws_bytes, void *stream);
+size_t edm_ccm_tables_workspace_bytes(int32_t N, int32_t L, int32_t tau, int32_t lag_min, int32_t lag_max);
+
 /* Scratch size in bytes for which = 0 (edm_simplex_optimal_E over N series) or
  * which = 1 (edm_ccm_all_pairs over an N-series dataset; E_max = largest E in E[]).
  * Returns 0 for invalid arguments. */
@@ -186,9 +225,9 @@ enum {
     EDM_PROF_PREP = 0,        /* transposes, padding, target ordering, centring, window sums, library sets */
     EDM_PROF_SIMPLEX_KNN = 1, /* phase-1 distance + select + forecast */
     EDM_PROF_SIMPLEX_RHO = 2, /* phase-1 Pearson + argmax */
-    EDM_PROF_CCM_KNN = 3,     /* phase-2 distance + select + weights -> tables */
+    EDM_PROF_CCM_KNN = 3,     /* phase-2 distance + select + fused weights -> tables */
     EDM_PROF_LOOKUP = 4,      /* phase-2 lookup + fused Pearson */
-    EDM_PROF_OTHER = 5        /* edm_embed_knn, convergence-test sample means */
+    EDM_PROF_OTHER = 5        /* edm_embed_knn, convergence-test sample means, table readback */
 };
 edm_status edm_profile_begin(void);
 edm_status edm_profile_end(double *ms, int64_t *launches);

@@ -513,6 +513,25 @@ static int knn_list(const double *x, int qlo, int qhi, const int *C, int nC, int
     return rc;
 }
 
+/* The table of one library series x over ONE convergence-test library set (the steps of
+ * convergence_row below for one (l, r, E), exposed so tests can compare the GPU's tables
+ * entry by entry): rows t in P_E = [(E-1)tau, L-1-Tp], candidates = the first min(l, n_E)
+ * labels of perm inside P_E (library_subset), minus t when exclude_self; the k = E+1 nearest
+ * by (d2, s) (C3, C4). Returns n_E, or OR_ETOOSHORT when the set leaves fewer than k. */
+int oracle_ccm_subset_table(const double *x, int L, int E, int tau, int Tp, int exclude_self,
+                            const int *perm, int l, int *idx, double *d2) {
+    if (E < 1 || tau < 1 || Tp < 0 || L < 2 || l < 1) return OR_EINVAL;
+    const int lo = (E - 1) * tau, hi = L - 1 - Tp;
+    if (hi < lo) return OR_ETOOSHORT;
+    int *C = (int *)malloc(sizeof(int) * L);
+    if (!C) return OR_ENOMEM;
+    const int nC = library_subset(perm, L, lo, hi, l, C);
+    int rc = (nC - (exclude_self ? 1 : 0) >= E + 1) ? knn_list(x, lo, hi, C, nC, E, tau, exclude_self, idx, d2)
+                                                  : OR_ETOOSHORT;
+    free(C);
+    return rc;
+}
+
 typedef struct {
     job_t base;
     const int *sizes; int nsizes;

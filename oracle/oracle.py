@@ -51,6 +51,8 @@ def lib():
         _lib.oracle_knn.argtypes = [dp, i, i, dp, i, i, i, i, i, ip, dp]
         _lib.oracle_ccm_table.restype = i
         _lib.oracle_ccm_table.argtypes = [dp, i, i, i, i, i, ip, dp, dp]
+        _lib.oracle_ccm_subset_table.restype = i
+        _lib.oracle_ccm_subset_table.argtypes = [dp, i, i, i, i, i, ip, i, ip, dp]
         _lib.oracle_xmap.restype = d
         _lib.oracle_xmap.argtypes = [ip, dp, i, i, i, dp, i, dp, dp]
         _lib.oracle_simplex_rho_E.restype = d
@@ -141,6 +143,21 @@ def ccm_table(x, E, tau=1, Tp=1, exclude_self=True):
                                   d2.ctypes.data_as(C.POINTER(C.c_double)), w.ctypes.data_as(C.POINTER(C.c_double))),
            "ccm_table")
     return idx, d2, w
+
+
+def ccm_subset_table(x, E, perm, l, tau=1, Tp=1, exclude_self=True):
+    """Table of one library series over one convergence-test library set (reading R16): the
+    first min(l, n_E) labels of perm inside P_E are the candidates. idx [n_E, E+1], d2 fp64."""
+    x, px = _d(x)
+    perm, pp = _i(perm)
+    L = len(x)
+    n = L - (E - 1) * tau - Tp
+    idx = np.zeros((max(n, 0), E + 1), np.int32)
+    d2 = np.zeros((max(n, 0), E + 1), np.float64)
+    _check(lib().oracle_ccm_subset_table(px, L, E, tau, Tp, int(exclude_self), pp, l,
+                                         idx.ctypes.data_as(C.POINTER(C.c_int)),
+                                         d2.ctypes.data_as(C.POINTER(C.c_double))), "ccm_subset_table")
+    return idx, d2
 
 
 def xmap(idx, w, t0, y, Tp=1):

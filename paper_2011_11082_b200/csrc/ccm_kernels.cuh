@@ -2,11 +2,12 @@
 //
 // Paper = PAPER.md; P:<line>. Kernel map:
 //   transpose_kernel      time-major [L][ld] -> series-major [n][L]           (S0 ingest)
-//   colprep_kernel        per-series fp64 mean and last-change index            (S5)
+//   scan_kernel           input check (finite, exactly rescalable), per-series   (S0/S5)
+//                         sweep exponent, fp64 mean and target exponent
 //   permute_kernel        centred, E-sorted, tile-padded time-major copy Yp     (S5)
 //   stats_kernel          per (E, column) fp64 sums of the observed window      (S5)
 //   knn_kernel<MODE>      fp64 incremental-over-E distances + warp top-(E+1)   (S1/S6/S7/S8)
-//                         MODE_CCM: weights -> table; MODE_SIMPLEX: forecast;
+//                         MODE_CCM: fused weights -> table; MODE_SIMPLEX: forecast;
 //                         MODE_EMBED: idx/dist/w of edm_embed_knn
 //   simplex_rho_kernel    two-pass fp64 Pearson of the phase-1 forecasts        (S2)
 //   argmax_kernel         optE = argmax_E rho(E)                                (S3)
@@ -53,13 +54,72 @@ __global__ void transpose_kernel(const float* __restrict__ in, int64_t ld, int L
 }
 
 // ------------------------------------------------------------------ S5 target preparation
-// mean[j] = fp64 mean of series j.
-__global__ void colprep_kernel(const float* __restrict__ y, int64_t ld, int N, int L, double* __restrict__ mean) {
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= N) return;
+// Exponent k of the exact power-of-two rescaling x * 2^k applied to a series before the
+// kNN sweep (reading R17): the fp32 prefilter's error bound needs squared
+// coordinate differences that neither overflow (|x| < 2^60 keeps sum_{m<20} (2 x)^2 < 2^127)
+// nor sit deep in the subnormal range, so a series whose max |x| lies outside [2^-40, 2^60)
+// is brought to [2^59, 2^60); every other series keeps k = 0. Distances scale by exactly
+// 2^2k (fp64 has no overflow/underflow for fp32 inputs), so selections are unchanged and the
+// stored distances are scaled back exactly.
+__host__ __device__ __forceinline__ int sweep_exponent(float mx) {
+    if (!(mx > 0.f)) return 0;
+    int e = 0;
+    (void)frexpf(mx, &e);  // mx in [2^(e-1), 2^e)
+    const int lg = e - 1;
+    return (lg >= 60 || lg < -40) ? 59 - lg : 0;
+}
+
+// S0 input check + S5 column statistics, one thread per series j in [c0, c0 + n) of the
+// time-major dataset (coalesced rows). Non-finite values are counted into bad[0] (the call
+// returns EINVAL: the paper's distances, and Pearson, are undefined for
+// them); a series whose sweep rescaling (sweep_exponent) would not be exact counts into bad[1]
+// (EUNSUPPORTED); bad[2] = smallest offending series index. sexp[j - c0] = sweep_exponent.
+// Optional (non-NULL): mean[j - c0] = fp64 mean (centring of the targets); texp[j - c0] =
+// exponent bringing max |x - mean| into [1, 2) when it lies outside [2^-30, 2^30) (the
+// lookup's fp32 moments; Pearson rho is scale-invariant), else 0.
+__global__ void scan_kernel(const float* __restrict__ y, int64_t ld, int c0, int n, int L,
+                            int* __restrict__ sexp, double* __restrict__ mean, int* __restrict__ texp,
+                            int* __restrict__ bad) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const float* col = y + c0 + j;
     double s = 0.0;
-    for (int t = 0; t < L; ++t) s += (double)y[(int64_t)t * ld + j];
-    mean[j] = s / L;
+    float mx = 0.f;
+    int nonfinite = 0;
+    for (int t = 0; t < L; ++t) {
+        const float v = col[(int64_t)t * ld];
+        if (!isfinite(v)) ++nonfinite;
+        else mx = fmaxf(mx, fabsf(v));
+        s += (double)v;
+    }
+    if (nonfinite) {
+        atomicAdd(bad, nonfinite);
+        atomicMin(bad + 2, c0 + j);
+        sexp[j] = 0;
+        if (mean) mean[j] = 0.0;
+        if (texp) texp[j] = 0;
+        return;
+    }
+    const int k = sweep_exponent(mx);
+    if (k < 0) {  // scaling down: exact unless a value would leave the normal fp32 range
+        const double sc = ldexp(1.0, k), inv = ldexp(1.0, -k);
+        bool exact = true;
+        for (int t = 0; t < L && exact; ++t) {
+            const float v = col[(int64_t)t * ld];
+            exact = (double)(float)((double)v * sc) * inv == (double)v;
+        }
+        if (!exact) { atomicAdd(bad + 1, 1); atomicMin(bad + 2, c0 + j); }
+    }
+    sexp[j] = k;
+    const double mu = s / L;
+    if (mean) mean[j] = mu;
+    if (texp) {
+        double mc = 0.0;
+        for (int t = 0; t < L; ++t) mc = fmax(mc, fabs((double)col[(int64_t)t * ld] - mu));
+        int e = 0;
+        if (mc > 0.0) { (void)frexp(mc, &e); --e; }
+        texp[j] = (mc > 0.0 && (e >= 30 || e < -30)) ? -e : 0;
+    }
 }
 
 // Yp = the centred targets in tile-major order: column p (tile p/32, lane p%32) at time t is
@@ -71,13 +131,14 @@ __host__ __device__ __forceinline__ int64_t yp_index(int p, int t, int L) {
 }
 __global__ void permute_kernel(const float* __restrict__ y, int64_t ld, int L, int Np,
                                const int* __restrict__ colmap, const double* __restrict__ mean,
-                               float* __restrict__ Yp) {
+                               const int* __restrict__ texp, float* __restrict__ Yp) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= Np) return;
     const int c = colmap[p];
     const double mu = c >= 0 ? mean[c] : 0.0;
+    const double sc = c >= 0 ? ldexp(1.0, texp[c]) : 1.0;  // texp = 0 for all but extreme-scale series
     for (int t = blockIdx.y; t < L; t += gridDim.y)
-        Yp[yp_index(p, t, L)] = c >= 0 ? (float)((double)y[(int64_t)t * ld + c] - mu) : 0.f;
+        Yp[yp_index(p, t, L)] = c >= 0 ? (float)(((double)y[(int64_t)t * ld + c] - mu) * sc) : 0.f;
 }
 
 // Observed-window statistics for every E: the observation of table row r
@@ -150,6 +211,13 @@ struct KnnParams {
     const float* Xpad;
     int64_t ldpad;
     int qpw;                // queries per warp of this launch (0: KNN_QPW)
+    // sweep rescaling (sweep_exponent): X row r is multiplied by 2^sexp[r] when the series is
+    // staged (sexp NULL: 2^sexp0 for every row); every stored distance is scaled back exactly
+    const int* sexp;
+    int sexp0;
+    // MODE_CCM table readback (edm_ccm_tables): fp32(sqrt(d2)) of every table entry, same
+    // layout as `tables` (NULL in the hot path)
+    float* tdist;
 };
 
 // knn_kernel series variants: shared-memory copy, shared-memory copy + library-set mask
@@ -187,10 +255,13 @@ __device__ __forceinline__ double simplex_weight(double d2, int k, int lane) {
 
 constexpr float THR_EMPTY = 3.402823466e38f;  // FLT_MAX: an empty list admits every finite candidate
 // fp32 prefilter bound of a fp64 list distance D: the sweep accumulates D in fp32, whose
-// relative error is below (E+3) 2^-24 < 2^-18 for E <= 20 (fp32 inputs, no overflow), so any
-// candidate with exact D_E <= D has fp32 D_E <= bound(D); the merge then decides exactly in fp64.
+// relative error is below (E+3) 2^-24 < 2^-18 for E <= 20 while the terms stay normal; terms
+// that fall into the subnormal range add at most 2^-150 each (E <= 20 of them: < 2^-140), and
+// the sweep rescaling (sweep_exponent) rules out overflow. So any candidate with exact
+// D_E <= D has fp32 D_E <= bound(D); the merge then decides exactly in fp64.
 __device__ __forceinline__ float prefilter_bound(double D) {
-    return D < 1e300 ? fminf(THR_EMPTY, __double2float_ru(__dmul_ru(D, 1.0 + 0x1p-18))) : THR_EMPTY;
+    return D < 1e300 ? fminf(THR_EMPTY, __double2float_ru(__dadd_ru(__dmul_ru(D, 1.0 + 0x1p-18), 0x1p-140)))
+                     : THR_EMPTY;
 }
 __host__ __device__ constexpr int knn_padl(int tau) { return (ECAP - 1) * tau; }
 constexpr int KNN_PADR = 32;
@@ -228,15 +299,17 @@ constexpr size_t knn_smem_bytes_gser(int L) { return (size_t)KNN_WARPS * knn_war
 __host__ __device__ constexpr int64_t knn_ldpad(int L, int tau) { return ((int64_t)knn_padl(tau) + L + KNN_PADR + 3) / 4 * 4; }
 
 // Padded global copies for KNN_GSER: out[b * ldpad + padl + t] = X[row_b * ldx + t] for
-// t in [0, L), 1e30 elsewhere (row_b = slot_series[b] or b).
+// t in [0, L), 1e30 elsewhere (row_b = slot_series[b] or b), rescaled by 2^sexp[row_b].
 __global__ void pad_series_kernel(const float* __restrict__ X, int64_t ldx, const int* __restrict__ slot_series,
-                                  int L, int padl, int64_t ldpad, int nslots, float* __restrict__ out) {
+                                  const int* __restrict__ sexp, int L, int padl, int64_t ldpad, int nslots,
+                                  float* __restrict__ out) {
     const int b = blockIdx.y;
     if (b >= nslots) return;
     const int row = slot_series ? slot_series[b] : b;
+    const double sc = ldexp(1.0, sexp[row]);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ldpad; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = i - padl;
-        out[(int64_t)b * ldpad + i] = (t >= 0 && t < L) ? X[(int64_t)row * ldx + t] : 1e30f;
+        out[(int64_t)b * ldpad + i] = (t >= 0 && t < L) ? (float)((double)X[(int64_t)row * ldx + t] * sc) : 1e30f;
     }
 }
 
@@ -330,7 +403,7 @@ template <int MODE, bool TAU1, bool FULLMASK, bool CMASK>
 __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, unsigned* memb, int mw,
                                          const float* __restrict__ qaf, const float* __restrict__ cbf,
                                          int t_begin, int t_end, int ncand, int ncl,
-                                         unsigned mask, int Etop, int b, int lane) {
+                                         unsigned mask, int Etop, int b, int lane, double unscale) {
     const int tau = TAU1 ? 1 : P.tau;
     const bool excl = (MODE != MODE_SIMPLEX) && P.excl;
     auto selected = [&](int e) { return FULLMASK || ((mask >> (e + 1)) & 1u); };
@@ -497,24 +570,46 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
             if (!selected(e)) continue;
             const int k = e + 2;
             const int row = t - e * tau;
-            const double d2 = lane < k ? W.D[loff(e) + lane] : CUDART_INF;
-            const int sl = lane < k ? W.S[loff(e) + lane] : 0;
+            double d2 = lane < k ? W.D[loff(e) + lane] : CUDART_INF;
+            int sl = lane < k ? W.S[loff(e) + lane] : 0;
+            // never store a sentinel: an entry still at its reset key (impossible for finite,
+            // validated input with >= E+1 candidates) becomes the query itself with a NaN
+            // distance, so its weights and every rho using the table are NaN, not garbage
+            const bool unfilled = lane < k && !(d2 < CUDART_INF);
+            if (unfilled) { sl = t; d2 = CUDART_NAN; }
+            const bool any_unfilled = __any_sync(FULL, unfilled);
             if (MODE == MODE_CCM) {
-                // {s + Tp, fp32 distance}; weights_kernel turns the distance into the weight
+                // S8 fused: weights of C5 from the Euclidean distances, fp32 exp and a
+                // tree sum (stored fp32); ratios d_j/d_1 are invariant under the sweep rescaling
                 const int kp = kpad(k);
+                float wv;
+                if (__any_sync(FULL, lane < k && d2 < 0x1p-100)) {
+                    wv = (float)simplex_weight<false>(d2, k, lane);  // tiny distances: fp64 ratios
+                } else {
+                    const float df = lane < k ? __fsqrt_rn(__double2float_rn(d2)) : 0.f;
+                    const float d1 = __shfl_sync(FULL, df, 0);
+                    float u = d1 > 0.f ? __expf(-__fdividef(df, d1)) : (df == 0.f ? 1.f : 0.f);
+                    u = lane < k ? fmaxf(u, 1e-6f) : 0.f;
+                    float sum = u;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+                    wv = u / sum;
+                }
+                if (any_unfilled) wv = CUDART_NAN_F;
                 if (lane < kp) {
-                    uint2 ent = lane < k ? make_uint2((unsigned)(sl + P.store_shift), __float_as_uint((float)sqrt(d2)))
-                                         : make_uint2(0u, 0u);
-                    P.tables[(int64_t)b * P.T_lib + P.offE[e + 1] + (int64_t)row * kp + lane] = ent;
+                    const int64_t o = (int64_t)b * P.T_lib + P.offE[e + 1] + (int64_t)row * kp + lane;
+                    P.tables[o] = lane < k ? make_uint2((unsigned)(sl + P.store_shift), __float_as_uint(wv))
+                                           : make_uint2(0u, 0u);
+                    if (P.tdist) P.tdist[o] = lane < k ? (float)(sqrt(d2) * unscale) : 0.f;
                 }
             } else if (MODE == MODE_EMBED) {
                 const double w = simplex_weight<true>(d2, k, lane);
                 if (lane < k) {
                     P.out_idx[(int64_t)row * k + lane] = sl;
-                    P.out_dist[(int64_t)row * k + lane] = (float)sqrt(d2);
+                    P.out_dist[(int64_t)row * k + lane] = (float)(sqrt(d2) * unscale);
                     if (P.out_w) P.out_w[(int64_t)row * k + lane] = (float)w;
                 }
-            } else {  // MODE_SIMPLEX: the (d2, s) list goes to forecast_kernel
+            } else {  // MODE_SIMPLEX: the (d2, s) list goes to forecast_kernel (ratios only: scale-free)
                 if (lane < k) {
                     const int64_t o = (int64_t)b * P.S_slot + P.offS[e + 1] + (int64_t)t * k + lane;
                     P.sd2[o] = d2;
@@ -542,15 +637,20 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnPa
     const int nx = padl + P.L + KNN_PADR;
     // the library series in shared memory, fp32 (the inputs are fp32: widening to fp64 where the
     // exact distances are formed is lossless), padded with 1e30 ((q - 1e30)^2 = +inf in fp32)
+    // sweep rescaling by 2^k (sweep_exponent; exact, validated by scan_kernel): distances are
+    // formed on the rescaled series and scaled back by 2^-k where they are stored
+    const int kexp = P.sexp ? P.sexp[row] : P.sexp0;
+    const double unscale = ldexp(1.0, -kexp);
     const float* xf_pad;
     if (GSER) {
-        xf_pad = P.Xpad + (int64_t)b * P.ldpad;
+        xf_pad = P.Xpad + (int64_t)b * P.ldpad;  // rescaled by pad_series_kernel
         (void)xg; (void)nx;
     } else {
+        const double sc = ldexp(1.0, kexp);
         float* xs = reinterpret_cast<float*>(knn_smem + (size_t)KNN_WARPS * knn_warp_bytes(P.L));
         for (int i = threadIdx.x; i < nx; i += blockDim.x) {
             const int t = i - padl;
-            xs[i] = (t >= 0 && t < P.L) ? xg[t] : 1e30f;
+            xs[i] = (t >= 0 && t < P.L) ? (kexp ? (float)((double)xg[t] * sc) : xg[t]) : 1e30f;
         }
         __syncthreads();
         xf_pad = xs;
@@ -587,49 +687,8 @@ __global__ void __launch_bounds__(KNN_WARPS * 32, KNN_MIN_CTAS) knn_kernel(KnnPa
     const int t0 = (blockIdx.x * KNN_WARPS + warp) * qpw;
     const int t1 = min(nq, t0 + qpw);
     const int ncl = CMASK ? __ldg(P.ncl) : 0;
-    if (t0 < t1) knn_warp<MODE, TAU1, FULLMASK, CMASK>(P, W, memb, mw, qaf, cbf, t0, t1, ncand, ncl, mask, Etop, b, lane);
-}
-
-// Weights of the phase-2 tables (S8, C5), one thread per table row: the kNN kernel
-// stored fp32(sqrt(d2)) (zero exactly when d2 is zero: the smallest nonzero d2 of fp32 data is
-// 2^-298, whose root 2^-149 is representable), here u_j = exp(-d_j/d_1) if d_1 > 0 else
-// [d_j == 0], floored at 1e-6 and normalised; stored as fp32 (rows of all selected E of the
-// block's libraries; row r of E starts at offE[E] + r * kpad(E+1) of library b's table).
-struct WeightParams {
-    uint2* tables;
-    int64_t T_lib;
-    int64_t offE[ECAP + 2];
-    int rowStart[ECAP + 2];  // cumulative row counts over the selected E (rowStart[ECAP+1] = total)
-    int nlib;
-    const int* slotE;        // library mode: only the rows of E = slotE[b] exist
-};
-__global__ void weights_kernel(WeightParams P) {
-    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int total = P.rowStart[ECAP + 1];
-    if (gid >= (int64_t)total * P.nlib) return;
-    const int b = (int)(gid / total);
-    const int r = (int)(gid - (int64_t)b * total);
-    int E = 1;
-    while (E <= ECAP && r >= P.rowStart[E + 1]) ++E;
-    if (P.slotE && P.slotE[b] != E) return;
-    const int k = E + 1, kp = kpad(k);
-    uint2* row = P.tables + (int64_t)b * P.T_lib + P.offE[E] + (int64_t)(r - P.rowStart[E]) * kp;
-    float d[ECAP + 1], u[ECAP + 1];
-    float sum = 0.f;
-    const float d1 = __uint_as_float(row[0].y);
-#pragma unroll
-    for (int j = 0; j < ECAP + 1; ++j) {
-        if (j < k) {
-            d[j] = __uint_as_float(row[j].y);
-            float v = d1 > 0.f ? __expf(-__fdividef(d[j], d1)) : (d[j] == 0.f ? 1.f : 0.f);
-            v = fmaxf(v, 1e-6f);
-            u[j] = v;
-            sum += v;
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < ECAP + 1; ++j)
-        if (j < k) row[j].y = __float_as_uint(u[j] / sum);
+    if (t0 < t1) knn_warp<MODE, TAU1, FULLMASK, CMASK>(P, W, memb, mw, qaf, cbf, t0, t1, ncand, ncl, mask, Etop, b, lane,
+                                                          unscale);
 }
 
 // ------------------------------------------------------------------ S2 / S3 phase-1 skill
@@ -907,20 +966,20 @@ template <bool SMEM>
 __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupParams P) {
     extern __shared__ __align__(16) unsigned char lk_smem[];
     // CTAs 0 .. ntiles-nsplit-1 take whole tiles from the last (target mode: highest E, the
-    // most expensive) down; the remaining nsplit cheapest tiles run as `parts` CTAs each, one per
-    // range of the block's libraries: two in the last wave of a large map (halves its imbalance),
-    // more when there are fewer tiles than SMs (small N)
-    int tile, b_lo = 0, b_hi = P.B;
+    // most expensive) down; the remaining nsplit cheapest tiles run as `parts` CTAs each, part p
+    // taking the rounds of 16 libraries m = p, p + parts, ... (strided, so that library mode's
+    // E-descending rounds spread over the parts): two in the last wave of a large map (halves its
+    // imbalance), more when there are fewer tiles than SMs (small N)
+    int tile, part = 0, parts = 1;
     {
         const int whole = P.ntiles - P.nsplit;
         if ((int)blockIdx.x < whole) {
             tile = P.ntiles - 1 - blockIdx.x;
         } else {
-            const int i = blockIdx.x - whole, part = i % P.parts;
-            const int per = (P.B + P.parts - 1) / P.parts;
+            const int i = blockIdx.x - whole;
+            part = i % P.parts;
+            parts = P.parts;
             tile = P.nsplit - 1 - i / P.parts;
-            b_lo = min(P.B, part * per);
-            b_hi = min(P.B, b_lo + per);
         }
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -948,7 +1007,7 @@ __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupPara
     ys = TILE_J;
     __syncthreads();
     const int col = P.colmap[tile * TILE_J + lane];
-    for (int b = b_lo + warp; b < b_hi; b += LOOKUP_WARPS) {
+    for (int b = part * LOOKUP_WARPS + warp; b < P.B; b += parts * LOOKUP_WARPS) {
         const int E = P.tileE ? Et : P.slotE[b];
         if (E > P.Eok) {
             if (col >= 0) P.rho[((int64_t)P.slotRow[b] - P.rbase) * P.rstride + P.roff + col] = CUDART_NAN_F;
@@ -1017,6 +1076,30 @@ __global__ void sample_mean_kernel(const float* __restrict__ src, int64_t s_stri
         if (!isnan(v)) { s += (double)v; ++cnt; }
     }
     dst[(int64_t)i * d_stride + j] = cnt ? (float)(s / cnt) : CUDART_NAN_F;
+}
+
+// ------------------------------------------------------------------ table readback (edm_ccm_tables)
+// Copies the rows of dimension E of library slots [0, nb) from the phase-2 tables (labels, fused
+// weights) and their fp32 distances (KnnParams.tdist) into idx/dist/w[(slotRow[b] * n + r) * k + j]
+// (k = E+1, n = table rows at E), adding label_shift to the labels. Library mode: only slots with
+// slotE[b] == E exist; the others are skipped.
+__global__ void table_extract_kernel(const uint2* __restrict__ tables, const float* __restrict__ tdist, int64_t T_lib,
+                                     int64_t offE, int n, int E, int nb, const int* __restrict__ slotRow,
+                                     const int* __restrict__ slotE, int label_shift, int* __restrict__ idx,
+                                     float* __restrict__ dist, float* __restrict__ w) {
+    const int k = E + 1, kp = kpad(k);
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= (int64_t)nb * n * k) return;
+    const int b = (int)(gid / ((int64_t)n * k));
+    const int rj = (int)(gid - (int64_t)b * n * k);
+    const int r = rj / k, j = rj % k;
+    if (slotE && slotE[b] != E) return;
+    const int64_t src = (int64_t)b * T_lib + offE + (int64_t)r * kp + j;
+    const int64_t dst = ((int64_t)slotRow[b] * n + r) * k + j;
+    const uint2 ent = tables[src];
+    idx[dst] = (int)ent.x + label_shift;
+    if (w) w[dst] = __uint_as_float(ent.y);
+    if (dist) dist[dst] = tdist[src];
 }
 
 }  // namespace ccm

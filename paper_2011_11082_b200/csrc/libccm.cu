@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -100,7 +101,8 @@ void table_layout(int L, int tau, int Tp, int64_t offE[ECAP + 2], int64_t* T_lib
     *T_lib = off;
 }
 
-constexpr int SIMPLEX_SLOTS = 1024;   // series per phase-1 block
+constexpr int SIMPLEX_SLOTS = 1024;   // series per phase-1 block (at most)
+constexpr size_t SIMPLEX_LIST_BUDGET = (size_t)16 << 30;  // phase-1 list bytes of one block (long series)
 constexpr int CCM_B = 16 * LOOKUP_WARPS;  // libraries per phase-2 block (16 per lookup warp)
 constexpr size_t CCM_TABLE_BUDGET = (size_t)24 << 30;  // table bytes of one block (long series)
 
@@ -115,6 +117,9 @@ constexpr int LOOKUP_SMEM_MAX = 227 * 1024;
 inline int64_t np_max(int N) { return (int64_t)(N + TILE_J - 1) / TILE_J * TILE_J + (int64_t)TILE_J * ECAP; }
 
 struct SimplexWs {
+    int SB;         // series per phase-1 block: SIMPLEX_SLOTS, fewer when the lists exceed the budget
+    int* sexp;      // [N] sweep exponents of the requested series (scan_kernel)
+    int* bad;       // [4] input-check counters (scan_kernel)
     float* Xs;      // [SB][L]
     double* pred;   // [SB][ECAP][LQ]
     double* rho;    // [SB][E_max]
@@ -129,7 +134,6 @@ struct SimplexWs {
 // Lists of every (E, target point): entries per slot = sum_E (E+1) * LQ.
 SimplexWs simplex_ws(void* base, int N, int L, int E_max, int tau) {
     SimplexWs w{};
-    const int SB = std::min(N, SIMPLEX_SLOTS);
     const int LQ = std::max(L / 2, 1);
     int64_t acc = 0;
     w.offS[0] = 0;
@@ -138,8 +142,14 @@ SimplexWs simplex_ws(void* base, int N, int L, int E_max, int tau) {
         if (E <= ECAP) acc += (int64_t)(E + 1) * LQ;
     }
     w.S_slot = acc;
+    const size_t per_slot = (size_t)L * sizeof(float) + (size_t)ECAP * LQ * sizeof(double) +
+                            (size_t)acc * (sizeof(double) + sizeof(int)) + (size_t)knn_ldpad(L, tau) * sizeof(float);
+    const int SB = (int)std::max<size_t>(1, std::min<size_t>({(size_t)N, (size_t)SIMPLEX_SLOTS, SIMPLEX_LIST_BUDGET / per_slot}));
+    w.SB = SB;
     size_t off = 0;
     char* b = (char*)base;
+    w.sexp = (int*)(b + off);   off += align_up((size_t)N * sizeof(int));
+    w.bad = (int*)(b + off);    off += align_up(4 * sizeof(int));
     w.Xs = (float*)(b + off);   off += align_up((size_t)SB * L * sizeof(float));
     w.pred = (double*)(b + off); off += align_up((size_t)SB * ECAP * LQ * sizeof(double));
     w.rho = (double*)(b + off);  off += align_up((size_t)SB * std::max(E_max, 1) * sizeof(double));
@@ -156,6 +166,9 @@ struct CcmWs {
     int* colmap;        // [Npm]
     int* tileE;         // [Npm / 32]
     double* mean;       // [N]
+    int* sexp;          // [N] sweep exponents (scan_kernel)
+    int* texp;          // [N] target exponents (scan_kernel)
+    int* bad;           // [4] input-check counters (scan_kernel)
     double2* stats;     // [nlag][ECAP][Npm] observed-window sums
     int* cflag;         // [nlag][ECAP][Npm] observed window constant
     int* slot_series;   // [N]
@@ -182,6 +195,9 @@ CcmWs ccm_ws(void* base, int N, int L, int Lk, int tau, int hrz, int nlag) {
     w.colmap = (int*)take((size_t)w.Npm * sizeof(int));
     w.tileE = (int*)take((size_t)(w.Npm / TILE_J) * sizeof(int));
     w.mean = (double*)take((size_t)N * sizeof(double));
+    w.sexp = (int*)take((size_t)N * sizeof(int));
+    w.texp = (int*)take((size_t)N * sizeof(int));
+    w.bad = (int*)take(4 * sizeof(int));
     w.stats = (double2*)take((size_t)nlag * ECAP * w.Npm * sizeof(double2));
     w.cflag = (int*)take((size_t)nlag * ECAP * w.Npm * sizeof(int));
     w.slot_series = (int*)take((size_t)N * sizeof(int));
@@ -279,14 +295,25 @@ bool knn_use_gser(int L, int tau) {
     return (size_t)KNN_MIN_CTAS * (knn_smem_bytes(L, tau) + 1024) > (size_t)228 * 1024;
 }
 
-// Lookup work split: the last nsplit tiles run as `parts` CTAs over library ranges -- one SM
+// Lookup work split: the last nsplit tiles run as `parts` CTAs over library sets -- one SM
 // count of tiles in halves for a large map, every tile in up to B/16 parts when there are fewer
-// tiles than two waves need (CCM_LK_SPLIT=n overrides nsplit, 0 = off).
-void lookup_split(int ntiles, int B, LookupParams& Q) {
-    int sms = 148, dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+// tiles than two waves need (CCM_LK_SPLIT=n overrides nsplit, 0 = off). `sms` / `env_split`
+// are queried once per call (split_config).
+struct SplitConfig {
+    int sms;
+    int env_split;  // -1: unset
+};
+SplitConfig split_config() {
+    SplitConfig c{148, -1};
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
     const char* env = getenv("CCM_LK_SPLIT");
-    int nsplit = env ? atoi(env) : sms;
+    if (env) c.env_split = atoi(env);
+    return c;
+}
+void lookup_split(int ntiles, int B, const SplitConfig& sc, LookupParams& Q) {
+    const int sms = sc.sms;
+    int nsplit = sc.env_split >= 0 ? sc.env_split : sms;
     nsplit = std::max(0, std::min(nsplit, ntiles));
     int parts = 2;
     if (ntiles < 2 * sms) parts = std::max(2, std::min(std::max(B / LOOKUP_WARPS, 1), (2 * sms + ntiles - 1) / std::max(ntiles, 1)));
@@ -296,12 +323,36 @@ void lookup_split(int ntiles, int B, LookupParams& Q) {
     Q.parts = parts;
 }
 
-edm_status pad_series(const float* X, int64_t ldx, const int* slot_series, int L, int tau, int nslots, float* out,
-                      cudaStream_t cs) {
+edm_status pad_series(const float* X, int64_t ldx, const int* slot_series, const int* sexp, int L, int tau, int nslots,
+                      float* out, cudaStream_t cs) {
     const int64_t ld = knn_ldpad(L, tau);
     dim3 grid((unsigned)std::min<int64_t>((ld + 255) / 256, 64), nslots);
-    PROF_LAUNCH(EDM_PROF_PREP, cs, pad_series_kernel<<<grid, 256, 0, cs>>>(X, ldx, slot_series, L, knn_padl(tau), ld, nslots, out));
+    PROF_LAUNCH(EDM_PROF_PREP, cs,
+                pad_series_kernel<<<grid, 256, 0, cs>>>(X, ldx, slot_series, sexp, L, knn_padl(tau), ld, nslots, out));
     LAUNCH_CHECK("pad_series_kernel");
+    return EDM_OK;
+}
+
+// S0 input check (scan_kernel) of series [c0, c0 + n): enqueue the scan and the copy of its
+// counters to `hbad` (host int[4]); the caller synchronises and calls check_bad.
+edm_status launch_scan(const edm_dataset& ds, int c0, int n, int* sexp, double* mean, int* texp, int* dbad, int* hbad,
+                       cudaStream_t cs) {
+    static const int init[4] = {0, 0, 0x7fffffff, 0};
+    CUDA_TRY(cudaMemcpyAsync(dbad, init, sizeof(init), cudaMemcpyHostToDevice, cs));
+    if (n > 0) {
+        PROF_LAUNCH(EDM_PROF_PREP, cs, scan_kernel<<<(n + 127) / 128, 128, 0, cs>>>(ds.data, ds.ld, c0, n, ds.L, sexp, mean, texp, dbad));
+        LAUNCH_CHECK("scan_kernel");
+    }
+    CUDA_TRY(cudaMemcpyAsync(hbad, dbad, 4 * sizeof(int), cudaMemcpyDeviceToHost, cs));
+    return EDM_OK;
+}
+edm_status check_bad(const int* hbad) {
+    if (hbad[0] > 0)
+        return fail(EDM_EINVAL, "the dataset holds %d non-finite value(s) (first in series %d): distances and rho are undefined",
+                    hbad[0], hbad[2]);
+    if (hbad[1] > 0)
+        return fail(EDM_EUNSUPPORTED, "series %d spans more than fp32's normal range after the exact power-of-two "
+                    "rescaling the kNN sweep needs (max |x| >= 2^60 together with values below ~2^-66)", hbad[2]);
     return EDM_OK;
 }
 
@@ -359,7 +410,25 @@ edm_status edm_embed_knn(const float* series, int32_t L, int32_t E, int32_t tau,
         return fail(EDM_EUNSUPPORTED, "edm_embed_knn stages the series in shared memory: L=%d tau=%d is too long", L, tau);
     edm_status st = check_device();
     if (st != EDM_OK) return st;
+    // input check and sweep exponent of the one series on the host (this inspection call has no
+    // workspace): one L-float copy and one stream synchronisation
+    int kexp = 0;
+    {
+        std::vector<float> h(L);
+        CUDA_TRY(cudaMemcpyAsync(h.data(), series, sizeof(float) * (size_t)L, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+        CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+        float mx = 0.f;
+        for (int t = 0; t < L; ++t) {
+            if (!std::isfinite(h[t])) return fail(EDM_EINVAL, "series[%d] is not finite", t);
+            mx = std::max(mx, std::fabs(h[t]));
+        }
+        kexp = sweep_exponent(mx);
+        for (int t = 0; t < L && kexp < 0; ++t)
+            if ((double)(float)std::ldexp((double)h[t], kexp) != std::ldexp((double)h[t], kexp))
+                return fail(EDM_EUNSUPPORTED, "series spans more than fp32's normal range after the sweep rescaling");
+    }
     KnnParams P{};
+    P.sexp0 = kexp;
     P.X = series;
     P.ldx = L;
     P.L = L; P.tau = tau; P.Tp = Tp; P.excl = exclude_self ? 1 : 0;
@@ -382,6 +451,14 @@ edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int
     if (s_begin == s_end) return EDM_OK;
     cudaStream_t cs = (cudaStream_t)stream;
     SimplexWs W = simplex_ws(workspace, ds.N, ds.L, E_max, tau);
+    {
+        int hbad[4];
+        st = launch_scan(ds, s_begin, s_end - s_begin, W.sexp, nullptr, nullptr, W.bad, hbad, cs);
+        if (st != EDM_OK) return st;
+        CUDA_TRY(cudaStreamSynchronize(cs));
+        st = check_bad(hbad);
+        if (st != EDM_OK) return st;
+    }
     const bool gser = knn_use_gser(ds.L, tau);
     const int L = ds.L, Llib = (L + 1) / 2, Ltgt = L - Llib;
     const int LQ = std::max(L / 2, 1);
@@ -392,7 +469,7 @@ edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int
         const int lo = (E - 1) * tau;
         if (Llib - 1 - lo >= E + 1 && Ltgt - 1 - lo >= 2) { mask |= 1u << E; Etop = E; }
     }
-    const int SB = std::min(ds.N, SIMPLEX_SLOTS);
+    const int SB = W.SB;
     for (int c0 = s_begin; c0 < s_end; c0 += SB) {
         const int nb = std::min(SB, s_end - c0);
         dim3 tb(32, 8), tg((nb + 31) / 32, (L + 31) / 32);
@@ -403,9 +480,10 @@ edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int
             P.X = W.Xs; P.ldx = L; P.L = L; P.tau = tau; P.Tp = 1; P.excl = 0;
             P.maskS = mask; P.Etop = Etop;
             P.sd2 = W.sd2; P.ss = W.ss; P.S_slot = W.S_slot;
+            P.sexp = W.sexp + (c0 - s_begin);
             memcpy(P.offS, W.offS, sizeof(W.offS));
             if (gser) {
-                st = pad_series(W.Xs, L, nullptr, L, tau, nb, W.Xpad, cs);
+                st = pad_series(W.Xs, L, nullptr, P.sexp, L, tau, nb, W.Xpad, cs);
                 if (st != EDM_OK) return st;
                 P.Xpad = W.Xpad; P.ldpad = knn_ldpad(L, tau);
             }
@@ -437,33 +515,39 @@ edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int
 
 namespace {
 
-// Weights of the rows of every E in maskS of nb library slots (S8).
-edm_status launch_weights(uint2* tables, int64_t T_lib, const int64_t offE[ECAP + 2], unsigned maskS, int Lk, int tau,
-                          int hrz, const int* slotE, int nb, cudaStream_t cs) {
-    WeightParams WP{};
-    WP.tables = tables; WP.T_lib = T_lib; WP.nlib = nb; WP.slotE = slotE;
-    memcpy(WP.offE, offE, sizeof(WP.offE));
-    int acc = 0;
-    for (int Ev = 1; Ev <= ECAP + 1; ++Ev) {
-        WP.rowStart[Ev] = acc;
-        if (Ev <= ECAP && ((maskS >> Ev) & 1u)) acc += (int)std::max<int64_t>(n_rows(Lk, Ev, tau, hrz), 0);
-    }
-    WP.rowStart[0] = 0;
-    const int64_t nthr = (int64_t)acc * nb;
+// Table readback (edm_ccm_tables): the rows of dimension Eq of every library built by the call
+// are copied out instead of running the lookup.
+struct TablesOut {
+    int Eq;
+    int32_t* idx;
+    float* dist;
+    float* w;
+};
+
+edm_status extract_tables(const TablesOut& to, const uint2* tables, const float* tdist, int64_t T_lib,
+                          const int64_t offE[ECAP + 2], int Lk, int tau, int hrz, int nb, const int* slot_row,
+                          const int* slotE, int label_shift, cudaStream_t cs) {
+    const int n = (int)n_rows(Lk, to.Eq, tau, hrz);
+    const int64_t nthr = (int64_t)nb * n * (to.Eq + 1);
     if (nthr == 0) return EDM_OK;
-    PROF_LAUNCH(EDM_PROF_CCM_KNN, cs, weights_kernel<<<(unsigned)((nthr + 255) / 256), 256, 0, cs>>>(WP));
-    LAUNCH_CHECK("weights_kernel");
+    PROF_LAUNCH(EDM_PROF_OTHER, cs,
+                table_extract_kernel<<<(unsigned)((nthr + 255) / 256), 256, 0, cs>>>(
+                    tables, tdist, T_lib, offE[to.Eq], n, to.Eq, nb, slot_row, slotE, label_shift, to.idx, to.dist, to.w));
+    LAUNCH_CHECK("table_extract_kernel");
     return EDM_OK;
 }
 
 // Convergence-test library blocks (reading R16): for every size l and sample r, tables over the
-// library set of (l, r) (knn_kernel<CMASK>), weights, one lookup pass writing the sample's rho,
-// then the mean over the R samples. E with l - exclude_self < E+1 have no table: rho = NaN.
+// library set of (l, r) (knn_kernel<CMASK>, weights fused), one lookup pass writing the sample's
+// rho, then the mean over the R samples. E with l - exclude_self < E+1 have no table: rho = NaN.
+// With `to` (edm_ccm_tables: one size, one sample) the tables are copied out instead.
 edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP + 2], int64_t T_lib, unsigned maskS,
-                       int Etop, int tau, int Tp, edm_e_mode mode, int exclude_self, int nlib, int ntiles, int Np,
-                       bool use_smem, size_t lk_smem, float* rho, void* conv_base, const ConvArgs& cv, cudaStream_t cs) {
+                       int tau, int Tp, edm_e_mode mode, int exclude_self, int lib_begin, int nlib, int ntiles, int Np,
+                       bool use_smem, size_t lk_smem, float* rho, void* conv_base, const ConvArgs& cv,
+                       const TablesOut* to, float* tdist, cudaStream_t cs) {
     const int N = ds.N, L = ds.L, R = cv.R, S = cv.nsizes, ncand = L - Tp;
     ConvWs C = conv_ws(conv_base, N, L, S, R, W.B);
+    const SplitConfig sc = split_config();
     CUDA_TRY(cudaMemcpyAsync(C.perms, cv.perms, sizeof(int) * (size_t)R * L, cudaMemcpyHostToDevice, cs));
     CUDA_TRY(cudaMemcpyAsync(C.sizes, cv.sizes, sizeof(int) * (size_t)S, cudaMemcpyHostToDevice, cs));
     const size_t sub_smem = (size_t)ncand * sizeof(unsigned);
@@ -486,23 +570,28 @@ edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP +
             const int64_t spitch = cv.rho_samples ? (int64_t)S * R * N : (int64_t)R * N;
             for (int r = 0; r < R; ++r) {
                 const int64_t qr = (int64_t)q * R + r;
-                if (whole && r > 0) {
+                if (whole && r > 0 && !to) {
                     CUDA_TRY(cudaMemcpy2DAsync(sbase + (int64_t)r * N, spitch * sizeof(float), sbase, spitch * sizeof(float),
                                                (size_t)N * sizeof(float), nb, cudaMemcpyDeviceToDevice, cs));
                     continue;
                 }
                 if (maskq) {
                     KnnParams P{};
-                    P.X = W.Xs; P.ldx = L; P.slot_series = W.slot_series + r0;
+                    P.X = W.Xs; P.ldx = L; P.slot_series = W.slot_series + r0; P.sexp = W.sexp + lib_begin;
                     P.L = L; P.tau = tau; P.Tp = Tp; P.store_shift = 0; P.excl = exclude_self ? 1 : 0;
                     P.maskS = maskq; P.Etop = Etopq; P.slotE = slotE;
-                    P.tables = W.tables; P.T_lib = T_lib;
+                    P.tables = W.tables; P.T_lib = T_lib; P.tdist = tdist;
                     memcpy(P.offE, offE, sizeof(P.offE));
                     P.allow = C.allow + qr * C.allow_ld; P.clist = C.clist + qr * L; P.ncl = C.ncl + qr;
                     edm_status st = launch_knn<MODE_CCM>(P, ncand, nb, cs);
                     if (st != EDM_OK) return st;
-                    st = launch_weights(W.tables, T_lib, offE, maskq, L, tau, Tp, slotE, nb, cs);
+                }
+                if (to) {
+                    if (to->Eq > Eok) return fail(EDM_EINVAL, "library size %d leaves fewer than E+1=%d neighbours", cv.sizes[q], to->Eq + 1);
+                    edm_status st = extract_tables(*to, W.tables, tdist, T_lib, offE, L, tau, Tp, nb, W.slot_row + r0,
+                                                   slotE, 0, cs);
                     if (st != EDM_OK) return st;
+                    continue;
                 }
                 LookupParams Q{};
                 Q.Yp = W.Yp; Q.Np = Np; Q.colmap = W.colmap;
@@ -513,7 +602,7 @@ edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP +
                 Q.stats = W.stats; Q.cflag = W.cflag;
                 Q.Lt = L; Q.Lk = L; Q.hrz = Tp; Q.gshift = Tp; Q.oshift = Tp;
                 Q.tau = tau; Q.B = nb; Q.N = N; Q.Eok = Eok;
-                lookup_split(ntiles, nb, Q);
+                lookup_split(ntiles, nb, sc, Q);
                 if (cv.rho_samples) {
                     Q.rho = cv.rho_samples; Q.rstride = (int64_t)S * R * N; Q.roff = qr * N; Q.rbase = 0;
                 } else {
@@ -523,6 +612,7 @@ edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP +
                 else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
                 LAUNCH_CHECK("lookup_kernel");
             }
+            if (to) continue;
             const int64_t nthr = (int64_t)nb * N;
             PROF_LAUNCH(EDM_PROF_OTHER, cs,
                         sample_mean_kernel<<<(unsigned)((nthr + 255) / 256), 256, 0, cs>>>(
@@ -533,23 +623,38 @@ edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP +
     return EDM_OK;
 }
 
-// Phase 2 core, shared by edm_ccm_all_pairs (one horizon Tp: m_lo = 0, m_hi = Tp, lags [Tp,Tp])
-// and edm_ccm_lagged (lags [lag_min, lag_max]). Tables are built once per library block on the
-// points t in [(E-1)tau + m_lo, L-1-m_hi] (the kNN runs on the series shifted by m_lo, with
-// horizon m_hi) and store the shifted label s - m_lo; each lag l is one lookup pass that reads
-// y[label + m_lo + l] and observes y[t + l]. rho[row * nlag*N + (l - lag_min) * N + j].
+// Bytes of the table-readback scratch after the phase-2 workspace (fp32 distances of a block).
+inline size_t tdist_bytes(const CcmWs& w) { return align_up((size_t)w.B * w.T_lib * sizeof(float)); }
+
+// Phase 2 core, shared by edm_ccm_all_pairs (one horizon Tp: m_lo = 0, m_hi = Tp, lags [Tp,Tp]),
+// edm_ccm_lagged (lags [lag_min, lag_max]), edm_ccm_convergence (cv) and edm_ccm_tables (to).
+// Tables are built once per library block on the points t in [(E-1)tau + m_lo, L-1-m_hi] (the
+// kNN runs on the series shifted by m_lo, with horizon m_hi) and store the shifted label
+// s - m_lo; each lag l is one lookup pass that reads y[label + m_lo + l] and observes y[t + l].
+// rho[row * nlag*N + (l - lag_min) * N + j].
 edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int m_hi, int lag_min, int lag_max,
                     edm_e_mode mode, int32_t exclude_self, int32_t lib_begin, int32_t lib_end, float* rho,
-                    void* workspace, size_t ws_bytes, size_t need, cudaStream_t cs, const ConvArgs* cv = nullptr) {
+                    void* workspace, size_t ws_bytes, size_t need, cudaStream_t cs, const ConvArgs* cv = nullptr,
+                    const TablesOut* to = nullptr) {
     if (need == 0 || ws_bytes < need) return fail(EDM_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
     edm_status st = check_device();
     if (st != EDM_OK) return st;
     const int N = ds.N, L = ds.L, Lk = L - m_lo, nlag = lag_max - lag_min + 1;
+    CcmWs W = ccm_ws(workspace, N, L, Lk, tau, m_hi, nlag);
+    char* extra = (char*)workspace + W.bytes;
+    float* tdist = nullptr;
+    if (to) { tdist = (float*)extra; extra += tdist_bytes(W); }
 
-    // ---- validate E[] and plan on the host (one small D2H copy)
+    // ---- S0 input check of the whole dataset (every series is a target) with the per-series
+    // sweep / target exponents and means; E[] is validated on the host: one synchronisation
+    int hbad[4];
+    st = launch_scan(ds, 0, N, W.sexp, W.mean, W.texp, W.bad, hbad, cs);
+    if (st != EDM_OK) return st;
     std::vector<int32_t> hE(N);
     CUDA_TRY(cudaMemcpyAsync(hE.data(), E, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, cs));
     CUDA_TRY(cudaStreamSynchronize(cs));
+    st = check_bad(hbad);
+    if (st != EDM_OK) return st;
     unsigned maskS = 0;
     int Etop = 0;
     for (int j = 0; j < N; ++j) {
@@ -561,8 +666,9 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
         maskS |= 1u << e;
         Etop = std::max(Etop, e);
     }
+    if (to && mode == EDM_E_TARGET && !((maskS >> to->Eq) & 1u))
+        return fail(EDM_EINVAL, "E=%d is not among E[]: target mode builds no table at it", to->Eq);
     if (lib_begin == lib_end) return EDM_OK;
-    CcmWs W = ccm_ws(workspace, N, L, Lk, tau, m_hi, nlag);
     int64_t offE[ECAP + 2], T_lib;
     table_layout(Lk, tau, m_hi, offE, &T_lib);
 
@@ -599,7 +705,7 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
         // library mode: a lookup warp handles slots w, w+16, ... of a block and its cost grows with
         // its libraries' E, so each block's libraries are sorted by E (descending, stable) and dealt
         // to the warps in snake order, which balances the 16 warps of every tile
-        const int B = ccm_block(T_lib);
+        const int B = W.B;
         for (int r0 = 0; r0 < nlib; r0 += B) {
             const int nb = std::min(B, nlib - r0);
             std::vector<int> ord(nb);
@@ -626,47 +732,51 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
         dim3 tb(32, 8), tg((nlib + 31) / 32, (L + 31) / 32);
         PROF_LAUNCH(EDM_PROF_PREP, cs, transpose_kernel<<<tg, tb, 0, cs>>>(ds.data, ds.ld, L, lib_begin, nlib, W.Xs));
         LAUNCH_CHECK("transpose_kernel");
-        PROF_LAUNCH(EDM_PROF_PREP, cs, colprep_kernel<<<(N + 127) / 128, 128, 0, cs>>>(ds.data, ds.ld, N, L, W.mean));
-        LAUNCH_CHECK("colprep_kernel");
-        dim3 pg((Np + 255) / 256, std::min(L, 256));
-        PROF_LAUNCH(EDM_PROF_PREP, cs, permute_kernel<<<pg, 256, 0, cs>>>(ds.data, ds.ld, L, Np, W.colmap, W.mean, W.Yp));
-        LAUNCH_CHECK("permute_kernel");
-        for (int l = lag_min; l <= lag_max; ++l) {
-            const int64_t so = (int64_t)(l - lag_min) * ECAP * W.Npm;
-            PROF_LAUNCH(EDM_PROF_PREP, cs,
-                        stats_kernel<<<(Np + 127) / 128, 128, 0, cs>>>(W.Yp, L, ds.data, ds.ld, W.colmap, Np, tau, m_lo + l,
-                                                                      L - 1 - m_hi + l, ECAP, W.stats + so, W.cflag + so));
-            LAUNCH_CHECK("stats_kernel");
+        if (!to) {
+            dim3 pg((Np + 255) / 256, std::min(L, 256));
+            PROF_LAUNCH(EDM_PROF_PREP, cs, permute_kernel<<<pg, 256, 0, cs>>>(ds.data, ds.ld, L, Np, W.colmap, W.mean, W.texp, W.Yp));
+            LAUNCH_CHECK("permute_kernel");
+            for (int l = lag_min; l <= lag_max; ++l) {
+                const int64_t so = (int64_t)(l - lag_min) * ECAP * W.Npm;
+                PROF_LAUNCH(EDM_PROF_PREP, cs,
+                            stats_kernel<<<(Np + 127) / 128, 128, 0, cs>>>(W.Yp, L, ds.data, ds.ld, W.colmap, Np, tau, m_lo + l,
+                                                                          L - 1 - m_hi + l, ECAP, W.stats + so, W.cflag + so));
+                LAUNCH_CHECK("stats_kernel");
+            }
         }
     }
 
-    // ---- library blocks: kNN tables (S6-S8) then one lookup + rho pass per lag (S9, S10)
+    // ---- library blocks: kNN tables with fused weights (S6-S8) then one lookup + rho pass per lag (S9, S10)
     const size_t tile_smem = (size_t)L * TILE_J * sizeof(float);
     const bool use_smem = tile_smem + lookup_ring_bytes() <= (size_t)LOOKUP_SMEM_MAX;
     const size_t lk_smem = (use_smem ? tile_smem : 0) + lookup_ring_bytes();
     if (use_smem) CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
     else CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
     const bool gser = knn_use_gser(Lk, tau);
-    if (cv) return conv_blocks(ds, W, offE, T_lib, maskS, Etop, tau, m_hi, mode, exclude_self, nlib, ntiles, Np,
-                               use_smem, lk_smem, rho, (char*)workspace + W.bytes, *cv, cs);
+    if (cv) return conv_blocks(ds, W, offE, T_lib, maskS, tau, m_hi, mode, exclude_self, lib_begin, nlib, ntiles, Np,
+                               use_smem, lk_smem, rho, extra, *cv, to, tdist, cs);
+    const SplitConfig sc = split_config();
     for (int r0 = 0; r0 < nlib; r0 += W.B) {
         const int nb = std::min(W.B, nlib - r0);
         KnnParams P{};
-        P.X = W.Xs + m_lo; P.ldx = L; P.slot_series = W.slot_series + r0;
+        P.X = W.Xs + m_lo; P.ldx = L; P.slot_series = W.slot_series + r0; P.sexp = W.sexp + lib_begin;
         P.L = Lk; P.tau = tau; P.Tp = m_hi; P.store_shift = 0; P.excl = exclude_self ? 1 : 0;
         P.maskS = maskS; P.Etop = Etop;
         P.slotE = (mode == EDM_E_LIBRARY) ? W.slotE + r0 : nullptr;
-        P.tables = W.tables; P.T_lib = T_lib;
+        P.tables = W.tables; P.T_lib = T_lib; P.tdist = tdist;
         memcpy(P.offE, offE, sizeof(offE));
         if (gser) {
-            st = pad_series(P.X, P.ldx, P.slot_series, Lk, tau, nb, W.Xpad, cs);
+            st = pad_series(P.X, P.ldx, P.slot_series, P.sexp, Lk, tau, nb, W.Xpad, cs);
             if (st != EDM_OK) return st;
             P.Xpad = W.Xpad; P.ldpad = knn_ldpad(Lk, tau);
         }
         st = launch_knn<MODE_CCM>(P, Lk - m_hi, nb, cs);
         if (st != EDM_OK) return st;
-        st = launch_weights(W.tables, T_lib, offE, maskS, Lk, tau, m_hi, P.slotE, nb, cs);
-        if (st != EDM_OK) return st;
+        if (to) {
+            st = extract_tables(*to, W.tables, tdist, T_lib, offE, Lk, tau, m_hi, nb, W.slot_row + r0, P.slotE, m_lo, cs);
+            if (st != EDM_OK) return st;
+            continue;
+        }
         for (int l = lag_min; l <= lag_max; ++l) {
             LookupParams Q{};
             Q.Yp = W.Yp; Q.Np = Np; Q.colmap = W.colmap;
@@ -680,7 +790,7 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
             Q.tau = tau; Q.B = nb; Q.N = N;
             Q.rho = rho; Q.rstride = (int64_t)nlag * N; Q.roff = (int64_t)(l - lag_min) * N;
             Q.rbase = 0; Q.Eok = ECAP;
-            lookup_split(ntiles, nb, Q);
+            lookup_split(ntiles, nb, sc, Q);
             if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
             else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
             LAUNCH_CHECK("lookup_kernel");
@@ -763,6 +873,49 @@ edm_status edm_ccm_convergence(edm_dataset ds, const int32_t* E, int32_t tau, in
     ConvArgs cv{lib_sizes, n_sizes, R, orders, rho_samples};
     return ccm_core(ds, E, tau, 0, Tp, Tp, Tp, mode, exclude_self, lib_begin, lib_end, rho, workspace, ws_bytes, need,
                     (cudaStream_t)stream, &cv);
+}
+
+size_t edm_ccm_tables_workspace_bytes(int32_t N, int32_t L, int32_t tau, int32_t lag_min, int32_t lag_max) {
+    if (N < 1 || L < 2 || tau < 1 || lag_min > lag_max) return 0;
+    const int m_lo = lag_min < 0 ? -lag_min : 0, m_hi = lag_max > 0 ? lag_max : 0;
+    if (m_lo + m_hi >= L) return 0;
+    const CcmWs w = ccm_ws(nullptr, N, L, L - m_lo, tau, m_hi, lag_max - lag_min + 1);
+    return w.bytes + tdist_bytes(w) + conv_ws(nullptr, N, L, 1, 1, w.B).bytes;
+}
+
+edm_status edm_ccm_tables(edm_dataset ds, const int32_t* E, int32_t tau, int32_t lag_min, int32_t lag_max,
+                          edm_e_mode mode, int32_t exclude_self, int32_t lib_size, const int32_t* order,
+                          int32_t lib_begin, int32_t lib_end, int32_t Eq, int32_t* idx, float* dist, float* w,
+                          void* workspace, size_t ws_bytes, void* stream) {
+    if (!ds.data || !E || !idx || !workspace) return fail(EDM_EINVAL, "null pointer");
+    if (ds.N < 1 || ds.L < 2 || ds.ld < ds.N || tau < 1 || lag_min > lag_max || Eq < 1 || Eq > ECAP ||
+        (mode != EDM_E_TARGET && mode != EDM_E_LIBRARY))
+        return fail(EDM_EINVAL, "bad arguments N=%d L=%d ld=%lld tau=%d lags [%d,%d] Eq=%d mode=%d", ds.N, ds.L,
+                    (long long)ds.ld, tau, lag_min, lag_max, Eq, (int)mode);
+    if (lib_begin < 0 || lib_end > ds.N || lib_begin > lib_end) return fail(EDM_EINVAL, "bad library range [%d,%d)", lib_begin, lib_end);
+    const int m_lo = lag_min < 0 ? -lag_min : 0, m_hi = lag_max > 0 ? lag_max : 0;
+    if (m_lo + m_hi >= ds.L) return fail(EDM_ETOOSHORT, "lag range [%d,%d] leaves no points at L=%d", lag_min, lag_max, ds.L);
+    const size_t need = edm_ccm_tables_workspace_bytes(ds.N, ds.L, tau, lag_min, lag_max);
+    TablesOut to{Eq, idx, dist, w};
+    if (!order)
+        return ccm_core(ds, E, tau, m_lo, m_hi, lag_min, lag_max, mode, exclude_self, lib_begin, lib_end, nullptr, workspace,
+                        ws_bytes, need, (cudaStream_t)stream, nullptr, &to);
+    // convergence-test library set (one size, one sample): single horizon Tp = lag_min = lag_max >= 0
+    if (lag_min != lag_max || lag_min < 0 || lib_size < 1)
+        return fail(EDM_EINVAL, "a library subset needs one horizon Tp = lag_min = lag_max >= 0 and lib_size >= 1");
+    {
+        std::vector<char> seen(ds.L, 0);
+        for (int i = 0; i < ds.L; ++i) {
+            const int v = order[i];
+            if (v < 0 || v >= ds.L || seen[v]) return fail(EDM_EINVAL, "order is not a permutation of 0..L-1");
+            seen[v] = 1;
+        }
+    }
+    if ((size_t)(ds.L - lag_min) * sizeof(unsigned) > (size_t)LOOKUP_SMEM_MAX || knn_smem_bytes(ds.L, tau) > (size_t)LOOKUP_SMEM_MAX)
+        return fail(EDM_EUNSUPPORTED, "library subsets: L=%d tau=%d exceeds the shared-memory series limit", ds.L, tau);
+    ConvArgs cv{&lib_size, 1, 1, order, nullptr};
+    return ccm_core(ds, E, tau, 0, lag_min, lag_min, lag_min, mode, exclude_self, lib_begin, lib_end, nullptr, workspace,
+                    ws_bytes, need, (cudaStream_t)stream, &cv, &to);
 }
 
 edm_status edm_causal_map_host(const float* host_data, int32_t N, int32_t L, int32_t E_max, int32_t tau, int32_t Tp,

@@ -10,6 +10,10 @@ Names follow the C ABI (PAPER.md problem statement P:316-317):
   simplex_optimal_E(data, E_max, tau)        -> optE[, rhoE]          (edm_simplex_optimal_E)
   ccm_all_pairs(data, E, tau, Tp, mode)      -> rho rows              (edm_ccm_all_pairs)
   causal_map_host(host array, ...)           -> optE, rho (numpy)     (edm_causal_map_host)
+  ccm_tables(data, E, Eq, ...)               -> idx, dist, w          (edm_ccm_tables, table readback)
+
+Workspaces are cached per (kind, device, stream): calls on different CUDA streams never
+share scratch memory (the C ABI is reentrant on distinct streams and workspaces).
 """
 from __future__ import annotations
 
@@ -29,7 +33,7 @@ E_CAP = 20
 EXPORTS = ("edm_embed_knn", "edm_simplex_optimal_E", "edm_ccm_all_pairs", "edm_workspace_bytes",
            "edm_causal_map_host", "edm_last_error", "edm_version", "edm_profile_begin", "edm_profile_end",
            "edm_ccm_lagged", "edm_ccm_lagged_workspace_bytes", "edm_ccm_convergence",
-           "edm_ccm_convergence_workspace_bytes")
+           "edm_ccm_convergence_workspace_bytes", "edm_ccm_tables", "edm_ccm_tables_workspace_bytes")
 PROF_KINDS = ("prep", "simplex_knn", "simplex_rho", "ccm_knn", "lookup", "other")
 
 
@@ -79,6 +83,11 @@ def load(path: Optional[str] = None):
                                         sz, vp]
     lib.edm_ccm_convergence_workspace_bytes.restype = sz
     lib.edm_ccm_convergence_workspace_bytes.argtypes = [i32, i32, i32, i32, i32, i32]
+    lib.edm_ccm_tables.restype = i32
+    lib.edm_ccm_tables.argtypes = [edm_dataset, vp, i32, i32, i32, i32, i32, i32, vp, i32, i32, i32, vp, vp, vp, vp, sz,
+                                   vp]
+    lib.edm_ccm_tables_workspace_bytes.restype = sz
+    lib.edm_ccm_tables_workspace_bytes.argtypes = [i32, i32, i32, i32, i32]
     lib.edm_profile_begin.restype = i32
     lib.edm_profile_begin.argtypes = []
     lib.edm_profile_end.restype = i32
@@ -114,17 +123,25 @@ def _dataset(data: torch.Tensor) -> edm_dataset:
 _ws_cache: dict = {}
 
 
-def workspace(which: int, N: int, L: int, E_max: int, tau: int, Tp: int, device) -> torch.Tensor:
-    nbytes = load().edm_workspace_bytes(which, N, L, E_max, tau, Tp)
-    if nbytes == 0:
-        raise EdmError(EDM_EINVAL, f"bad workspace request which={which} N={N} L={L} E_max={E_max}")
-    key = (which, torch.device(device))
+def _workspace_for(kind, nbytes: int, device) -> torch.Tensor:
+    """Scratch of at least nbytes for `kind` on torch's current stream of `device`. Cached per
+    (kind, device, stream) and allocated while that stream is current, so a buffer is only ever
+    used on the stream the caching allocator associates it with."""
+    device = torch.device(device)
+    key = (kind, device, torch.cuda.current_stream(device).cuda_stream)
     ws = _ws_cache.get(key)
     if ws is None or ws.numel() < nbytes:
         _ws_cache.pop(key, None)
         ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
         _ws_cache[key] = ws
     return ws
+
+
+def workspace(which: int, N: int, L: int, E_max: int, tau: int, Tp: int, device) -> torch.Tensor:
+    nbytes = load().edm_workspace_bytes(which, N, L, E_max, tau, Tp)
+    if nbytes == 0:
+        raise EdmError(EDM_EINVAL, f"bad workspace request which={which} N={N} L={L} E_max={E_max}")
+    return _workspace_for(which, nbytes, device)
 
 
 def release_workspaces():
@@ -209,24 +226,10 @@ def ccm_lagged(data: torch.Tensor, E: torch.Tensor, tau: int = 1, lag_min: int =
     nbytes = load().edm_ccm_lagged_workspace_bytes(ds.N, ds.L, tau, lag_min, lag_max)
     if nbytes == 0:
         raise EdmError(EDM_EINVAL, f"bad lagged workspace request N={ds.N} L={ds.L} lags=[{lag_min},{lag_max}]")
-    key = ("lagged", torch.device(data.device))
-    ws = _ws_cache.get(key)
-    if ws is None or ws.numel() < nbytes:
-        _ws_cache.pop(key, None)
-        ws = torch.empty(nbytes, dtype=torch.uint8, device=data.device)
-        _ws_cache[key] = ws
+    ws = _workspace_for("lagged", nbytes, data.device)
     _check(load().edm_ccm_lagged(ds, E.data_ptr(), tau, lag_min, lag_max, _mode(mode), int(exclude_self), lib_begin,
                                  lib_end, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(data.device)))
     return out
-
-
-def _workspace_for(key, nbytes: int, device) -> torch.Tensor:
-    ws = _ws_cache.get(key)
-    if ws is None or ws.numel() < nbytes:
-        _ws_cache.pop(key, None)
-        ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
-        _ws_cache[key] = ws
-    return ws
 
 
 def ccm_convergence(data: torch.Tensor, E: torch.Tensor, lib_sizes, orders, tau: int = 1, Tp: int = 1,
@@ -252,12 +255,51 @@ def ccm_convergence(data: torch.Tensor, E: torch.Tensor, lib_sizes, orders, tau:
     nbytes = load().edm_ccm_convergence_workspace_bytes(ds.N, ds.L, tau, Tp, len(sizes), R)
     if nbytes == 0:
         raise EdmError(EDM_EINVAL, f"bad convergence workspace request N={ds.N} L={ds.L} sizes={len(sizes)} R={R}")
-    ws = _workspace_for(("convergence", torch.device(data.device)), nbytes, data.device)
+    ws = _workspace_for("convergence", nbytes, data.device)
     _check(load().edm_ccm_convergence(ds, E.data_ptr(), tau, Tp, _mode(mode), int(exclude_self),
                                       sizes.ctypes.data, len(sizes), orders.ctypes.data, R, lib_begin, lib_end,
                                       out.data_ptr(), smp.data_ptr() if samples else None, ws.data_ptr(), ws.numel(),
                                       _stream(data.device)))
     return (out, smp) if samples else out
+
+
+def ccm_tables(data: torch.Tensor, E: torch.Tensor, Eq: int, tau: int = 1, lag_min: int = 1,
+               lag_max: Optional[int] = None, mode="target", exclude_self: bool = True, lib_begin: int = 0,
+               lib_end: Optional[int] = None, lib_size: int = 0, order=None, with_dist: bool = True,
+               with_weights: bool = True):
+    """Phase-2 table readback (edm_ccm_tables): the tables of dimension Eq exactly as the hot path
+    builds them, for library rows [lib_begin, lib_end) -> idx int32 [rows, n, Eq+1], dist, w fp32
+    (None unless requested). lag_min = lag_max = Tp is the single-horizon table; order (host int32
+    [L]) + lib_size select one convergence-test library set. Library mode: rows of libraries whose
+    E differs from Eq are left at -1 / NaN."""
+    ds = _dataset(data)
+    _require_cuda(E, torch.int32, "E")
+    E = E.contiguous()
+    if E.numel() != ds.N:
+        raise ValueError("E must have N entries")
+    lag_max = lag_min if lag_max is None else lag_max
+    lib_end = ds.N if lib_end is None else lib_end
+    rows = max(lib_end - lib_begin, 0)
+    m_lo, m_hi = max(0, -lag_min), max(0, lag_max)
+    n = max(ds.L - (Eq - 1) * tau - m_lo - m_hi, 0)
+    idx = torch.full((rows, n, Eq + 1), -1, dtype=torch.int32, device=data.device)
+    dist = torch.full((rows, n, Eq + 1), float("nan"), dtype=torch.float32, device=data.device) if with_dist else None
+    w = torch.full((rows, n, Eq + 1), float("nan"), dtype=torch.float32, device=data.device) if with_weights else None
+    ordp = None
+    if order is not None:
+        order = np.ascontiguousarray(np.asarray(order, dtype=np.int32).ravel())
+        if order.size != ds.L:
+            raise ValueError("order must hold L labels")
+        ordp = order.ctypes.data
+    nbytes = load().edm_ccm_tables_workspace_bytes(ds.N, ds.L, tau, lag_min, lag_max)
+    if nbytes == 0:
+        raise EdmError(EDM_EINVAL, f"bad tables workspace request N={ds.N} L={ds.L} lags=[{lag_min},{lag_max}]")
+    ws = _workspace_for("tables", nbytes, data.device)
+    _check(load().edm_ccm_tables(ds, E.data_ptr(), tau, lag_min, lag_max, _mode(mode), int(exclude_self), lib_size,
+                                 ordp, lib_begin, lib_end, Eq, idx.data_ptr(),
+                                 dist.data_ptr() if dist is not None else None, w.data_ptr() if w is not None else None,
+                                 ws.data_ptr(), ws.numel(), _stream(data.device)))
+    return idx, dist, w
 
 
 def causal_map(data: torch.Tensor, E_max: int = 20, tau: int = 1, Tp: int = 1, mode="target",

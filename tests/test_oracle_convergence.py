@@ -102,3 +102,32 @@ def test_bad_orders_rejected():
         O.ccm_convergence_rows(data, E, [10], bad)
     with pytest.raises(ValueError):
         O.ccm_convergence_rows(data, E, [0], synth.library_orders(1, 40, 0))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_subset_table_matches_bruteforce(seed):
+    # oracle_ccm_subset_table (the per-(l, r, E) table of reading R16, exposed for the GPU table
+    # readback parity) against the numpy brute force: library set by masking, full lexsort
+    rng = np.random.default_rng(700 + seed)
+    L = int(rng.integers(50, 90))
+    x = synth.random_dataset(4, L, seed)[:, seed % 4].astype(float)  # column 0 is quantised (ties)
+    perm = synth.library_orders(1, L, seed)[0]
+    tau, Tp = 1 + seed % 2, seed % 3
+    for E in (1, 2, 4):
+        for l in (E + 3, 20, L):
+            for excl in (True, False):
+                P = np.arange((E - 1) * tau, L - Tp)
+                C = np.sort(perm[(perm >= P[0]) & (perm <= P[-1])][:l])
+                idx, d2 = O.ccm_subset_table(x, E, perm, l, tau, Tp, excl)
+                ridx, _ = nn_weights(embed(x, E, tau, P), embed(x, E, tau, C), C, E + 1,
+                                     excl_times=P if excl else None)
+                np.testing.assert_array_equal(idx, ridx)
+                # the distances are the plain fp64 sums of C3 (brute force in the same order)
+                Q, Cm = embed(x, E, tau, P), embed(x, E, tau, idx.ravel())
+                ref = np.zeros(idx.size)
+                for m in range(E):
+                    diff = np.repeat(Q[:, m], E + 1) - Cm[:, m]
+                    ref = ref + diff * diff
+                np.testing.assert_array_equal(d2.ravel(), ref)
+    with pytest.raises(ValueError):  # |C| - 1 < E + 1
+        O.ccm_subset_table(x, 3, perm, 4, 1, 1, True)
