@@ -138,20 +138,30 @@ def lookup_pipe_cycles(E: np.ndarray, L: int, tau: int, Tp: int, mode: str) -> f
     return float(sum(ntiles * n(int(e)) * row(int(e)) for e in E))
 
 
-def knn_fp64_ops(E: np.ndarray, L: int, tau: int, Tp: int, mode: str, lib_size: int | None = None) -> float:
-    """Algorithmic fp64 operations of the phase-2 distance pass: for each library, every
-    ordered pair (t, s != t) of P_E at every E up to the largest needed E costs one
-    subtract, multiply and add (incremental over E). With a library set of size
-    lib_size (convergence test) the candidates per query are min(lib_size, n_E)."""
+def knn_updates(E: np.ndarray, L: int, tau: int, Tp: int, mode: str, lib_size: int | None = None) -> float:
+    """Algorithmic (pair, E) updates of the phase-2 distance pass: for each
+    library, every ordered pair (t, s != t) of P_E at every E up to the largest needed E
+    (incremental over E); each update is 2 FP32 lane-operations in the sweep (the
+    difference and the fused multiply-add). With a library set of size lib_size (convergence
+    test) the candidates per query are min(lib_size, n_E)."""
     def per_lib(etop):
         tot = 0.0
         for e in range(1, etop + 1):
             n = L - (e - 1) * tau - Tp
-            tot += n * ((n if lib_size is None else min(lib_size, n)) - 1) * 3.0
+            tot += n * ((n if lib_size is None else min(lib_size, n)) - 1)
         return tot
     if mode == "target":
         return len(E) * per_lib(int(E.max()))
     return float(sum(per_lib(int(e)) for e in E))
+
+
+def load_onchip():
+    """Measured on-chip peaks (tools/onchip_peaks.cu on a B200 of this pool, profiles/onchip_peaks.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "onchip_peaks.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
 
 
 def load_peaks():
@@ -276,40 +286,71 @@ def oracle_sample(data, E, mode, tau, Tp, n_lib, n_series, lags=None, conv=None,
     return N * N * nlag / full, t2 - t0, cores, desc
 
 
+# Sample sizes of the oracle timing, shared by the main arm's cpu_baseline and --impl reference
+# (the same sampler, the same sizes, the same E source: one number, measured twice).
+ORACLE_SAMPLE_LIBS, ORACLE_SAMPLE_SERIES = 128, 256
+
+
+def oracle_E(config, data, cfg):
+    """The E vector the oracle's phase-2 sample uses: the ORACLE's own optimal E of every series
+    (tests/golden/<config>_optE_oracle.npz, written by tools/oracle_full_optE.py, which calls only
+    oracle/) when it exists for this exact workload; otherwise the oracle's phase 1 on the first
+    ORACLE_SAMPLE_SERIES series with the rest drawn (seeded) from that empirical distribution."""
+    L, N = data.shape
+    path = os.path.join(ROOT, "tests", "golden", f"{config}_optE_oracle.npz")
+    if os.path.exists(path):
+        z = np.load(path)
+        if int(z["N"]) == N and int(z["L"]) == L:
+            return z["optE"].astype(np.int32), f"oracle optE of all {N} series ({os.path.relpath(path, ROOT)})"
+    from oracle import oracle as O
+    ns = min(N, ORACLE_SAMPLE_SERIES)
+    Es, _ = O.simplex_all(data, cfg["E_max"], cfg["tau"], 0, ns)
+    E_all = np.random.default_rng(synth.SEED_BASE).choice(Es, N).astype(np.int32)
+    E_all[:ns] = Es
+    return E_all, f"oracle optE of {ns} series, the other {N - ns} drawn from their distribution"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def run_reference(args):
-    """--impl reference: the fp64 oracle on the host cores (rank 0 only), same config/metric."""
+    """--impl reference: the fp64 oracle on the host cores (rank 0 only), same config/metric.
+    Each step times the oracle on a bounded sample of the workload (oracle_sample, the sampler of
+    the main arm's cpu_baseline); the reported value is the median over steps of the full-map rate
+    EXTRAPOLATED from the sample (per-library time x N / threads), labelled as such."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cfg = synth.CONFIGS[args.config]
     data = synth.make_config(args.config, N=args.N, L=args.L)
     L, N = data.shape
-    from oracle import oracle as O
-    n_series = min(N, 64)
-    n_lib = min(N, args.cpu_sample or 48)
-    # E for the phase-2 sample: the oracle's own phase 1 on the whole set would be too slow at
-    # c3; use E from the oracle on the sampled series for those, and the sample's mode for the rest
-    # phase 2 needs every target's E; the oracle's phase 1 over all N series would take far
-    # longer than the bounded sample, so the unsampled targets draw E (seeded) from the
-    # empirical distribution of the sampled series' oracle E
-    Es, _ = O.simplex_all(data, cfg["E_max"], cfg["tau"], 0, n_series)
-    E_all = np.random.default_rng(synth.SEED_BASE).choice(Es, N).astype(np.int32)
-    E_all[:n_series] = Es
-    times = []
-    for _ in range(args.warmup):
-        pass  # the oracle has no warm-up state; W is accepted for the contract
-    value = None
-    for _ in range(args.steps):
-        v, secs, cores, desc = oracle_sample(data, E_all, args.mode, cfg["tau"], cfg["Tp"], n_lib, n_series)
-        times.append(secs)
-        value = v if value is None else min(value, v)
+    E_all, e_src = oracle_E(args.config, data, cfg)
+    n_lib = min(N, args.cpu_sample or ORACLE_SAMPLE_LIBS)
+    values, secs_each = [], []
+    desc, cores = "", 0
+    for _ in range(args.steps):  # the oracle has no warm-up state; W is accepted for the contract
+        v, secs, cores, desc = oracle_sample(data, E_all, args.mode, cfg["tau"], cfg["Tp"], n_lib,
+                                             min(N, ORACLE_SAMPLE_SERIES))
+        values.append(v)
+        secs_each.append(secs)
+    value = float(statistics.median(values))
+    sample = f"{desc}; E: {e_src}; median of {args.steps} step(s)"
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * N * N / value,
+        "extrapolated": True, "measured_seconds_per_step": secs_each,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {N} series x L={L}, E=1..{cfg['E_max']}, tau={cfg['tau']}, "
                                f"Tp={cfg['Tp']}, mode={args.mode}", "N": N, "L": L},
-        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
+                         "extrapolated": True, "sample": sample},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
@@ -364,29 +405,25 @@ def main():
         nlag = len(conv_sizes) * args.samples  # cross maps per (library, target) pair
     rho_rows = torch.empty((per, nlag, N) if lags else (per, N), dtype=torch.float32, device=dev)
     gather_list = [torch.empty_like(rho_rows) for _ in range(world)] if (rank == 0 and world > 1) else None
-    Ebuf = torch.zeros(per, dtype=torch.int32, device=dev)
-    Eall = torch.empty(per * world, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step(ev=None):
         if ev:
             ev[0].record(stream)
         optE = libccm.simplex_optimal_E(data, E_max, tau, s0, s1)           # S1-S3
-        Ebuf[: optE.numel()] = optE
         if ev:
             ev[1].record(stream)
-        if world > 1:
-            dist.all_gather_into_tensor(Eall, Ebuf)                          # S4 (NCCL)
-            E = torch.cat([Eall[r * per: r * per + (distributed.shard(N, r, world)[1] -
-                                                      distributed.shard(N, r, world)[0])] for r in range(world)])
-        else:
-            E = Ebuf[:N]
+        E = distributed.all_gather_E(optE, N) if world > 1 else optE         # S4 (NCCL all-gather)
         if ev:
             ev[2].record(stream)
         if lags:
             libccm.ccm_lagged(data, E, tau, lags[0], lags[1], args.mode, True, l0, l1, out=rho_rows)  # f1
         elif conv:
             libccm.ccm_convergence(data, E, conv[0], conv[1], tau, Tp, args.mode, True, l0, l1)  # f2
+        elif args.mode == "library" and world > 1:
+            # library mode: rows dealt round-robin over the E-sorted order
+            rows = distributed.assign_rows(E, world, "library")[rank]
+            libccm.ccm_rows(data, E, rows, tau, Tp, "library", True, out=rho_rows)  # S5-S9
         else:
             libccm.ccm_all_pairs(data, E, tau, Tp, args.mode, True, l0, l1, out=rho_rows)  # S5-S9
         if ev:
@@ -469,8 +506,8 @@ def main():
         "kernel": "lookup_kernel (S9: gather-weighted lookup + fused Pearson)",
         "bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
         "frac": (achieved / smem_peak) if achieved else None, "traffic": traffic,
-        "peak_source": f"derived: {nsm} SMs x 128 B/clk x {sm_max_mhz:.0f} MHz (B300_MICROARCH smem crossbar; no "
-                       "measured smem peak in MEASURED_PEAKS.json)",
+        "peak_source": f"derived: {nsm} SMs x 128 B/clk x {sm_max_mhz:.0f} MHz (B300_MICROARCH smem crossbar; "
+                       "MEASURED_PEAKS.json has no smem figure -- the measured one is peak_measured)",
         "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_s * 1e3, "launches": lk_n,
         "share_of_step": lk_ms / ms_local if ms_local else None,
         "pipe_model": {"frac": (lookup_pipe_cycles(E_host, L, tau, Tp, args.mode) * rows_frac * nlag * args.steps /
@@ -489,22 +526,33 @@ def main():
             if not len(sub):
                 return 0.0
             if args.mode == "target":  # every library builds tables up to the largest admitted E
-                return knn_fp64_ops(sub[:1] * 0 + sub.max(), L, tau, Tp, "target", l) * N
-            return knn_fp64_ops(sub, L, tau, Tp, "library", l)
-        knn_ops = sum(conv_ops(l) for l in conv[0]) * args.samples * rows_frac
+                return knn_updates(sub[:1] * 0 + sub.max(), L, tau, Tp, "target", l) * N
+            return knn_updates(sub, L, tau, Tp, "library", l)
+        knn_upd = sum(conv_ops(l) for l in conv[0]) * args.samples * rows_frac
     else:
-        knn_ops = knn_fp64_ops(E_host, L, tau, Tp, args.mode) * rows_frac
-    fp64_peak = nsm * 64.0 * sm_max_mhz * 1e6 / 1e12  # Tops/s: 64 fp64 lanes/clk/SM (measured, tools/microbench)
+        knn_upd = knn_updates(E_host, L, tau, Tp, args.mode) * rows_frac
+    onchip = load_onchip()
+    fp32_peak = nsm * 128.0 * sm_max_mhz * 1e6 / 1e12  # T lane-ops/s: 128 FP32 lanes/clk/SM (4 x 32 per SM)
+    kn_ach = knn_upd * 2.0 * args.steps / (kn_ms / 1e3) / 1e12 if kn_n else None
     roofline_knn = {
-        "kernel": "knn_kernel<CCM> (S6-S8: fp64 incremental distances + warp top-k + weights)",
-        "bound": "alu", "unit": "Tops/s (fp64 sub/mul/add)",
-        "peak_source": f"derived: {nsm} SMs x 64 fp64 lanes/clk x {sm_max_mhz:.0f} MHz (64/clk/SM measured by "
-                       "tools/microbench.cu on this B200); algorithmic = 3 fp64 ops per (pair, E) update",
-        "achieved": knn_ops * args.steps / (kn_ms / 1e3) / 1e12 if kn_n else None, "peak": fp64_peak,
-        "frac": (knn_ops * args.steps / (kn_ms / 1e3) / 1e12 / fp64_peak) if kn_n else None,
+        "kernel": "phase-2 kNN (S6-S8: incremental fp32 distance sweep + exact fp64 selection + fused weights)",
+        "bound": "alu", "unit": "T FP32 lane-ops/s",
+        "peak_source": f"derived: {nsm} SMs x 128 FP32 lanes/clk x {sm_max_mhz:.0f} MHz (B200_PROFILING unit counts); "
+                       "algorithmic = 2 FP32 ops (difference, fused multiply-add) per (pair, E) update",
+        "algorithmic_updates_per_step": knn_upd,
+        "achieved": kn_ach, "peak": fp32_peak, "frac": (kn_ach / fp32_peak) if kn_ach else None,
+        "peak_measured": (onchip["fp32_ffma_lanes_per_clk_sm"] * nsm * sm_max_mhz * 1e6 / 1e12
+                          if onchip.get("fp32_ffma_lanes_per_clk_sm") else None),
         "avg_launch_ms": kn_ms / max(kn_n, 1), "launches": kn_n,
         "share_of_step": kn_ms / ms_local if ms_local else None,
     }
+    if roofline_knn["peak_measured"] and kn_ach:
+        roofline_knn["frac_measured"] = kn_ach / roofline_knn["peak_measured"]
+    if onchip.get("smem_bytes_per_clk_sm") and achieved:
+        smem_meas = onchip["smem_bytes_per_clk_sm"] * nsm * sm_max_mhz * 1e6 / 1e9
+        roofline["peak_measured"] = smem_meas
+        roofline["frac_measured"] = achieved / smem_meas
+        roofline["peak_measured_source"] = "profiles/onchip_peaks.json (tools/onchip_peaks.cu, best conflict-free LDS)"
     launches = sum(n for _, n in prof.values())
     # the dominant kernel (largest share of the step) carries "roofline"; the other is kept beside it
     knn_traffic = load_traffic().get("ccm_knn_dram_bytes_per_launch")
@@ -553,9 +601,12 @@ def main():
     cpu = None
     unit = "(pair, lag)/s" if lags else "(pair, size, sample)/s" if conv else "pairs/s"
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_lib = args.cpu_sample or (min(N, 128) if not conv else min(N, max(16, 128 // nlag)))
-        v, secs, cores, desc = oracle_sample(host, E_host, args.mode, tau, Tp, n_lib, min(N, 256), lags, conv)
-        cpu = {"value": v, "unit": unit, "cores": cores, "kind": "oracle", "sample": desc}
+        n_lib = args.cpu_sample or (min(N, ORACLE_SAMPLE_LIBS) if not conv else min(N, max(16, ORACLE_SAMPLE_LIBS // nlag)))
+        E_or, e_src = oracle_E(args.config, host, cfg) if (args.N is None and args.L is None) else (E_host, "the run's E")
+        v, secs, cores, desc = oracle_sample(host, E_or, args.mode, tau, Tp, n_lib, min(N, ORACLE_SAMPLE_SERIES), lags,
+                                             conv)
+        cpu = {"value": v, "unit": unit, "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
+               "extrapolated": True, "sample": f"{desc}; E: {e_src}"}
 
     # ---- fast host implementation (the CPU side of the paper's GPU-vs-CPU
     # comparison; bit-identical to the oracle), same bounded-sample method

@@ -124,6 +124,15 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t *E, int32_t tau, int3
                              int32_t lib_end, float *rho, void *workspace, size_t ws_bytes,
                              void *stream);
 
+/* Phase 2 for an arbitrary LIST of library rows (the same computation as edm_ccm_all_pairs; used to
+ * deal library rows to GPUs by E in library mode, where a library's cost grows with its own E,
+ * SURVEY 8(e)): rho[r * N + j] = skill of cross-mapping series j from series lib_list[r].
+ *   lib_list : HOST int32[nlib], each in [0, N) (duplicates allowed).
+ * Same workspace (edm_workspace_bytes(1, ...)), conventions and errors as edm_ccm_all_pairs. */
+edm_status edm_ccm_rows(edm_dataset ds, const int32_t *E, int32_t tau, int32_t Tp, edm_e_mode mode,
+                        int32_t exclude_self, const int32_t *lib_list, int32_t nlib, float *rho, void *workspace,
+                        size_t ws_bytes, void *stream);
+
 /* Time-delay cross mapping ("The adjacency in the network is determined
  * by time delay cross mapping"): the phase-2 map at every lag l in [lag_min, lag_max] (l may be
  * negative) from ONE set of kNN tables per library block. Tables are built on the points

@@ -36,21 +36,29 @@ enum { MODE_CCM = 0, MODE_SIMPLEX = 1, MODE_EMBED = 2 };
 __host__ __device__ constexpr int kpad(int k) { return (k + 1) & ~1; }
 
 // ------------------------------------------------------------------ S0 ingest
-// out[c][t] = in[t * ld + c0 + c] for c < ncols; 32x32 tiles through shared memory.
+// out[c][t] = in[t * ld + col(c)] for c < ncols, col(c) = cols[c] (a library list) or c0 + c;
+// 32x32 tiles through shared memory.
 __global__ void transpose_kernel(const float* __restrict__ in, int64_t ld, int L, int c0, int ncols,
-                                 float* __restrict__ out) {
+                                 float* __restrict__ out, const int* __restrict__ cols = nullptr) {
     __shared__ float tile[32][33];
     const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
     const int cb = blockIdx.x * 32, tb = blockIdx.y * 32;
+    const int col = cb + tx < ncols ? (cols ? cols[cb + tx] : c0 + cb + tx) : 0;
     for (int i = ty; i < 32; i += 8) {
         int t = tb + i, c = cb + tx;
-        tile[i][tx] = (t < L && c < ncols) ? in[(int64_t)t * ld + c0 + c] : 0.f;
+        tile[i][tx] = (t < L && c < ncols) ? in[(int64_t)t * ld + col] : 0.f;
     }
     __syncthreads();
     for (int i = ty; i < 32; i += 8) {
         int c = cb + i, t = tb + tx;
         if (c < ncols && t < L) out[(int64_t)c * L + t] = tile[tx][i];
     }
+}
+
+// out[i] = in[idx[i]], i < n
+__global__ void gather_int_kernel(const int* __restrict__ in, const int* __restrict__ idx, int n, int* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = in[idx[i]];
 }
 
 // ------------------------------------------------------------------ S5 target preparation

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "ccm_kernels.cuh"
+#include "knn_eseq.cuh"
 #include "libccm.h"
 
 using namespace ccm;
@@ -169,6 +170,8 @@ struct CcmWs {
     int* sexp;          // [N] sweep exponents (scan_kernel)
     int* texp;          // [N] target exponents (scan_kernel)
     int* bad;           // [4] input-check counters (scan_kernel)
+    int* libidx;        // [N] series of library row r (edm_ccm_rows' list)
+    int* rsexp;         // [N] sweep exponent of library row r (list order)
     double2* stats;     // [nlag][ECAP][Npm] observed-window sums
     int* cflag;         // [nlag][ECAP][Npm] observed window constant
     int* slot_series;   // [N]
@@ -198,6 +201,8 @@ CcmWs ccm_ws(void* base, int N, int L, int Lk, int tau, int hrz, int nlag) {
     w.sexp = (int*)take((size_t)N * sizeof(int));
     w.texp = (int*)take((size_t)N * sizeof(int));
     w.bad = (int*)take(4 * sizeof(int));
+    w.libidx = (int*)take((size_t)N * sizeof(int));
+    w.rsexp = (int*)take((size_t)N * sizeof(int));
     w.stats = (double2*)take((size_t)nlag * ECAP * w.Npm * sizeof(double2));
     w.cflag = (int*)take((size_t)nlag * ECAP * w.Npm * sizeof(int));
     w.slot_series = (int*)take((size_t)N * sizeof(int));
@@ -263,6 +268,39 @@ edm_status launch_knn_m(const KnnParams& P, dim3 grid, size_t smem, bool full, c
     return full ? launch_knn_t<MODE, false, true, VAR>(P, grid, smem, st) : launch_knn_t<MODE, false, false, VAR>(P, grid, smem, st);
 }
 
+// E-sequential kNN (knn_eseq.cuh): used when every E in 1..Etop is selected (target mode,
+// phase 1), the candidates fit the register chunks (ncand <= 32 ESQ_NCMAX) and no candidate
+// mask / global series copy is involved; CCM_KNN_ALGO=sweep forces knn_kernel (measurements).
+#ifndef CCM_ESQ_QPW
+#define CCM_ESQ_QPW 32
+#endif
+template <int MODE, bool TAU1, int NC>
+edm_status launch_esq_t(const KnnParams& P, dim3 grid, cudaStream_t st) {
+    const size_t smem = esq_smem_bytes(P.tau, NC, P.L);
+    if (smem > 48 * 1024)
+        CUDA_TRY(cudaFuncSetAttribute(knn_eseq_kernel<MODE, TAU1, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PROF_LAUNCH(MODE == MODE_CCM ? EDM_PROF_CCM_KNN : EDM_PROF_SIMPLEX_KNN, st,
+                knn_eseq_kernel<MODE, TAU1, NC><<<grid, ESQ_WARPS * 32, smem, st>>>(P));
+    LAUNCH_CHECK("knn_eseq_kernel");
+    return EDM_OK;
+}
+template <int MODE, bool TAU1>
+edm_status launch_esq_nc(const KnnParams& P, int nch, dim3 grid, cudaStream_t st) {
+    if (nch <= 8) return launch_esq_t<MODE, TAU1, 8>(P, grid, st);
+    if (nch <= 16) return launch_esq_t<MODE, TAU1, 16>(P, grid, st);
+    if (nch <= 24) return launch_esq_t<MODE, TAU1, 24>(P, grid, st);
+    if (nch <= 32) return launch_esq_t<MODE, TAU1, 32>(P, grid, st);
+    if (nch <= 40) return launch_esq_t<MODE, TAU1, 40>(P, grid, st);
+    return launch_esq_t<MODE, TAU1, 48>(P, grid, st);
+}
+template <int MODE>
+bool esq_eligible(const KnnParams& P, bool full, int ncand) {
+    const char* env = getenv("CCM_KNN_ALGO");
+    if (env && !strcmp(env, "sweep")) return false;
+    return full && !P.slotE && !P.allow && !P.Xpad && ncand >= 1 && ncand <= 32 * ESQ_NCMAX &&
+           esq_smem_bytes(P.tau, ESQ_NCMAX, P.L) <= (size_t)227 * 1024;
+}
+
 // Picks the specialisation: tau == 1 (constant-offset shared loads), whether every E in
 // 1..Etop is selected (no per-E membership test), and the series variant: library-set mask
 // (phase 2 convergence test, P.allow), padded global series (P.Xpad, long series), else the
@@ -272,10 +310,22 @@ edm_status launch_knn(const KnnParams& P0, int nq, int slots, cudaStream_t st) {
     // the fewest CTAs of KNN_QPW-query warps, then the run length that spreads the queries
     // evenly over them (no nearly idle last CTA: 1449 queries -> 16 CTAs of 4 x 23)
     KnnParams P = P0;
+    const bool full = !P.slotE && P.Etop >= 1 && P.maskS == ((2u << P.Etop) - 2u);
+    if constexpr (MODE != MODE_EMBED) {
+        const int ncand = MODE == MODE_SIMPLEX ? (P.L + 1) / 2 - 1 : P.L - P.Tp;
+        if (esq_eligible<MODE>(P, full, ncand)) {
+            const char* qenv = getenv("CCM_ESQ_QPW");
+            const int qmax = qenv ? std::max(1, atoi(qenv)) : CCM_ESQ_QPW;
+            const int nc = std::max(1, (nq + ESQ_WARPS * qmax - 1) / (ESQ_WARPS * qmax));
+            P.qpw = std::max(1, (nq + nc * ESQ_WARPS - 1) / (nc * ESQ_WARPS));
+            dim3 g((nq + ESQ_WARPS * P.qpw - 1) / (ESQ_WARPS * P.qpw), slots);
+            const int nch = (ncand + 31) / 32;
+            return P.tau == 1 ? launch_esq_nc<MODE, true>(P, nch, g, st) : launch_esq_nc<MODE, false>(P, nch, g, st);
+        }
+    }
     const int ncta = std::max(1, (nq + KNN_QPB - 1) / KNN_QPB);
     P.qpw = std::max(1, (nq + ncta * KNN_WARPS - 1) / (ncta * KNN_WARPS));
     dim3 grid((nq + KNN_WARPS * P.qpw - 1) / (KNN_WARPS * P.qpw), slots);
-    const bool full = !P.slotE && P.Etop >= 1 && P.maskS == ((2u << P.Etop) - 2u);
     if constexpr (MODE == MODE_CCM) {
         if (P.allow) return launch_knn_m<MODE, KNN_CMASK>(P, grid, knn_smem_bytes(P.L, P.tau), full, st);
     }
@@ -542,7 +592,7 @@ edm_status extract_tables(const TablesOut& to, const uint2* tables, const float*
 // rho, then the mean over the R samples. E with l - exclude_self < E+1 have no table: rho = NaN.
 // With `to` (edm_ccm_tables: one size, one sample) the tables are copied out instead.
 edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP + 2], int64_t T_lib, unsigned maskS,
-                       int tau, int Tp, edm_e_mode mode, int exclude_self, int lib_begin, int nlib, int ntiles, int Np,
+                       int tau, int Tp, edm_e_mode mode, int exclude_self, const int* row_sexp, int nlib, int ntiles, int Np,
                        bool use_smem, size_t lk_smem, float* rho, void* conv_base, const ConvArgs& cv,
                        const TablesOut* to, float* tdist, cudaStream_t cs) {
     const int N = ds.N, L = ds.L, R = cv.R, S = cv.nsizes, ncand = L - Tp;
@@ -577,7 +627,7 @@ edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP +
                 }
                 if (maskq) {
                     KnnParams P{};
-                    P.X = W.Xs; P.ldx = L; P.slot_series = W.slot_series + r0; P.sexp = W.sexp + lib_begin;
+                    P.X = W.Xs; P.ldx = L; P.slot_series = W.slot_series + r0; P.sexp = row_sexp;
                     P.L = L; P.tau = tau; P.Tp = Tp; P.store_shift = 0; P.excl = exclude_self ? 1 : 0;
                     P.maskS = maskq; P.Etop = Etopq; P.slotE = slotE;
                     P.tables = W.tables; P.T_lib = T_lib; P.tdist = tdist;
@@ -635,7 +685,7 @@ inline size_t tdist_bytes(const CcmWs& w) { return align_up((size_t)w.B * w.T_li
 edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int m_hi, int lag_min, int lag_max,
                     edm_e_mode mode, int32_t exclude_self, int32_t lib_begin, int32_t lib_end, float* rho,
                     void* workspace, size_t ws_bytes, size_t need, cudaStream_t cs, const ConvArgs* cv = nullptr,
-                    const TablesOut* to = nullptr) {
+                    const TablesOut* to = nullptr, const int32_t* lib_list = nullptr) {
     if (need == 0 || ws_bytes < need) return fail(EDM_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
     edm_status st = check_device();
     if (st != EDM_OK) return st;
@@ -697,10 +747,11 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
     }
     const int ntiles = (int)tileE.size();
     const int Np = ntiles * TILE_J;
-    // library slots
+    // library slots: row r of this call is series lib(r) = lib_list[r] (edm_ccm_rows) or lib_begin + r
     const int nlib = lib_end - lib_begin;
+    auto lib = [&](int r) { return lib_list ? lib_list[r] : lib_begin + r; };
     std::vector<int> sser(nlib), srow(nlib), sE(nlib);
-    for (int r = 0; r < nlib; ++r) { sser[r] = r; srow[r] = r; sE[r] = hE[lib_begin + r]; }
+    for (int r = 0; r < nlib; ++r) { sser[r] = r; srow[r] = r; sE[r] = hE[lib(r)]; }
     if (mode == EDM_E_LIBRARY) {
         // library mode: a lookup warp handles slots w, w+16, ... of a block and its cost grows with
         // its libraries' E, so each block's libraries are sorted by E (descending, stable) and dealt
@@ -710,14 +761,14 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
             const int nb = std::min(B, nlib - r0);
             std::vector<int> ord(nb);
             for (int i = 0; i < nb; ++i) ord[i] = r0 + i;
-            std::stable_sort(ord.begin(), ord.end(), [&](int a, int c) { return hE[lib_begin + a] > hE[lib_begin + c]; });
+            std::stable_sort(ord.begin(), ord.end(), [&](int a, int c) { return hE[lib(a)] > hE[lib(c)]; });
             for (int p = 0; p < nb; ++p) {
                 const int m = p / LOOKUP_WARPS, j = p % LOOKUP_WARPS;
                 const bool full_round = (m + 1) * LOOKUP_WARPS <= nb;
                 const int slot = r0 + m * LOOKUP_WARPS + ((m & 1) && full_round ? LOOKUP_WARPS - 1 - j : j);
                 sser[slot] = ord[p];
                 srow[slot] = ord[p];
-                sE[slot] = hE[lib_begin + ord[p]];
+                sE[slot] = hE[lib(ord[p])];
             }
         }
     }
@@ -726,11 +777,19 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
     CUDA_TRY(cudaMemcpyAsync(W.slot_series, sser.data(), sizeof(int) * nlib, cudaMemcpyHostToDevice, cs));
     CUDA_TRY(cudaMemcpyAsync(W.slot_row, srow.data(), sizeof(int) * nlib, cudaMemcpyHostToDevice, cs));
     CUDA_TRY(cudaMemcpyAsync(W.slotE, sE.data(), sizeof(int) * nlib, cudaMemcpyHostToDevice, cs));
+    const int* row_sexp = W.sexp + lib_begin;
+    if (lib_list) {
+        CUDA_TRY(cudaMemcpyAsync(W.libidx, lib_list, sizeof(int) * nlib, cudaMemcpyHostToDevice, cs));
+        PROF_LAUNCH(EDM_PROF_PREP, cs, gather_int_kernel<<<(nlib + 255) / 256, 256, 0, cs>>>(W.sexp, W.libidx, nlib, W.rsexp));
+        LAUNCH_CHECK("gather_int_kernel");
+        row_sexp = W.rsexp;
+    }
 
     // ---- ingest and target preparation (S0, S5); one set of window statistics per lag
     {
         dim3 tb(32, 8), tg((nlib + 31) / 32, (L + 31) / 32);
-        PROF_LAUNCH(EDM_PROF_PREP, cs, transpose_kernel<<<tg, tb, 0, cs>>>(ds.data, ds.ld, L, lib_begin, nlib, W.Xs));
+        PROF_LAUNCH(EDM_PROF_PREP, cs, transpose_kernel<<<tg, tb, 0, cs>>>(ds.data, ds.ld, L, lib_begin, nlib, W.Xs,
+                                                                           lib_list ? W.libidx : nullptr));
         LAUNCH_CHECK("transpose_kernel");
         if (!to) {
             dim3 pg((Np + 255) / 256, std::min(L, 256));
@@ -753,13 +812,13 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
     if (use_smem) CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
     else CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
     const bool gser = knn_use_gser(Lk, tau);
-    if (cv) return conv_blocks(ds, W, offE, T_lib, maskS, tau, m_hi, mode, exclude_self, lib_begin, nlib, ntiles, Np,
+    if (cv) return conv_blocks(ds, W, offE, T_lib, maskS, tau, m_hi, mode, exclude_self, row_sexp, nlib, ntiles, Np,
                                use_smem, lk_smem, rho, extra, *cv, to, tdist, cs);
     const SplitConfig sc = split_config();
     for (int r0 = 0; r0 < nlib; r0 += W.B) {
         const int nb = std::min(W.B, nlib - r0);
         KnnParams P{};
-        P.X = W.Xs + m_lo; P.ldx = L; P.slot_series = W.slot_series + r0; P.sexp = W.sexp + lib_begin;
+        P.X = W.Xs + m_lo; P.ldx = L; P.slot_series = W.slot_series + r0; P.sexp = row_sexp;
         P.L = Lk; P.tau = tau; P.Tp = m_hi; P.store_shift = 0; P.excl = exclude_self ? 1 : 0;
         P.maskS = maskS; P.Etop = Etop;
         P.slotE = (mode == EDM_E_LIBRARY) ? W.slotE + r0 : nullptr;
@@ -813,6 +872,21 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int3
     const size_t need = edm_workspace_bytes(1, ds.N, ds.L, ECAP, tau, Tp);
     return ccm_core(ds, E, tau, 0, Tp, Tp, Tp, mode, exclude_self, lib_begin, lib_end, rho, workspace, ws_bytes, need,
                     (cudaStream_t)stream);
+}
+
+edm_status edm_ccm_rows(edm_dataset ds, const int32_t* E, int32_t tau, int32_t Tp, edm_e_mode mode,
+                        int32_t exclude_self, const int32_t* lib_list, int32_t nlib, float* rho, void* workspace,
+                        size_t ws_bytes, void* stream) {
+    if (!ds.data || !E || !rho || !workspace || (nlib > 0 && !lib_list)) return fail(EDM_EINVAL, "null pointer");
+    if (ds.N < 1 || ds.L < 2 || ds.ld < ds.N || tau < 1 || Tp < 0 || nlib < 0 || nlib > ds.N ||
+        (mode != EDM_E_TARGET && mode != EDM_E_LIBRARY))
+        return fail(EDM_EINVAL, "bad arguments N=%d L=%d ld=%lld tau=%d Tp=%d nlib=%d mode=%d", ds.N, ds.L, (long long)ds.ld,
+                    tau, Tp, nlib, (int)mode);
+    for (int r = 0; r < nlib; ++r)
+        if (lib_list[r] < 0 || lib_list[r] >= ds.N) return fail(EDM_EINVAL, "lib_list[%d]=%d outside [0,%d)", r, lib_list[r], ds.N);
+    const size_t need = edm_workspace_bytes(1, ds.N, ds.L, ECAP, tau, Tp);
+    return ccm_core(ds, E, tau, 0, Tp, Tp, Tp, mode, exclude_self, 0, nlib, rho, workspace, ws_bytes, need,
+                    (cudaStream_t)stream, nullptr, nullptr, lib_list);
 }
 
 size_t edm_ccm_lagged_workspace_bytes(int32_t N, int32_t L, int32_t tau, int32_t lag_min, int32_t lag_max) {

@@ -6,7 +6,9 @@ Partitioning (the paper's inter-node scheme P:535-551 with stati
   * the ONE data-path exchange: all-gather of optE (N int32) -- the paper's "master
     broadcasts optE to all workers" -- since phase 2 on every rank needs the
     E of every target;
-  * phase 2: library rows are split into contiguous blocks -> rho rows [rows, N];
+  * phase 2: library rows are split into contiguous blocks in target mode (uniform cost) and
+    dealt round-robin over an E-sorted order in library mode (cost grows with the library's E)
+    -> rho rows [rows, N] (assign_rows);
   * result assembly: gather of the rho row blocks to rank 0 (replaces the per-element HDF5
     writes of P:553-563).
 The kernels are deterministic and each rho[i, j] is computed identically whichever rank
@@ -19,6 +21,7 @@ from __future__ import annotations
 
 from typing import Callable, Optional
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -45,21 +48,41 @@ def all_gather_E(local: torch.Tensor, N: int, group=None) -> torch.Tensor:
     return torch.cat(parts)
 
 
-def gather_rows(local: torch.Tensor, N: int, dst: int = 0, group=None) -> Optional[torch.Tensor]:
-    """Gather rho row blocks [rows_r, N] to rank dst -> [N, N] there (None elsewhere)."""
+def assign_rows(E, world: int, mode) -> list:
+    """Library rows of every rank (phase 2), identical on every rank (computed from E[], no
+    exchange). Target mode: contiguous blocks (a library's cost does not depend on its own E:
+    every library builds the tables of every E in S). Library mode: the table is built at the
+    library's own E, so its cost grows with E_i; rows are sorted by E descending (stable) and dealt
+    round-robin, rank r taking positions r, r + world, ..., each list ascending."""
+    E = np.asarray(E.cpu() if hasattr(E, "cpu") else E)
+    N = E.shape[0]
+    if mode in ("library", 1):
+        order = np.argsort(-E.astype(np.int64), kind="stable")
+        return [np.sort(order[r::world]).astype(np.int32) for r in range(world)]
+    return [np.arange(*shard(N, r, world), dtype=np.int32) for r in range(world)]
+
+
+def _is_range(rows: np.ndarray) -> bool:
+    return rows.size == 0 or (rows[-1] - rows[0] + 1 == rows.size and np.all(np.diff(rows) == 1))
+
+
+def gather_rows(local: torch.Tensor, rows_all: list, N: int, dst: int = 0, group=None) -> Optional[torch.Tensor]:
+    """Gather every rank's rho rows (local [len(rows_all[rank]), N]) to rank dst -> the [N, N] map
+    there, row i at its library index (None elsewhere)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    per = -(-N // world)
+    per = max(max(len(r) for r in rows_all), 1)
     buf = torch.full((per, N), float("nan"), dtype=local.dtype, device=local.device)
     buf[: local.shape[0]] = local
     if rank == dst:
         gl = [torch.empty_like(buf) for _ in range(world)]
         dist.gather(buf, gl, dst=dst, group=group)
-        rows = []
+        full = torch.empty((N, N), dtype=local.dtype, device=local.device)
         for r in range(world):
-            b, e = shard(N, r, world)
-            rows.append(gl[r][: e - b])
-        return torch.cat(rows)
+            rows = rows_all[r]
+            if rows.size:
+                full[torch.from_numpy(rows.astype(np.int64)).to(local.device)] = gl[r][: rows.size]
+        return full
     dist.gather(buf, None, dst=dst, group=group)
     return None
 
@@ -67,7 +90,8 @@ def gather_rows(local: torch.Tensor, N: int, dst: int = 0, group=None) -> Option
 def run(data: torch.Tensor, E_max: int, tau: int, Tp: int, mode, exclude_self: bool,
         simplex_fn: Callable, ccm_fn: Callable, gather: bool = True, group=None, timers: Optional[dict] = None):
     """Sharded causal map. simplex_fn(data, E_max, tau, s_begin, s_end) -> optE shard;
-    ccm_fn(data, E, tau, Tp, mode, exclude_self, lib_begin, lib_end) -> rho rows.
+    ccm_fn(data, E, tau, Tp, mode, exclude_self, rows) -> rho rows of the libraries `rows`
+    (an ascending int32 array from assign_rows).
     Returns (E[N], rho rows of this rank, full rho on rank 0 if gather else None)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
@@ -75,9 +99,9 @@ def run(data: torch.Tensor, E_max: int, tau: int, Tp: int, mode, exclude_self: b
     s0, s1 = shard(N, rank, world)
     optE_local = simplex_fn(data, E_max, tau, s0, s1)
     E = all_gather_E(optE_local, N, group)
-    l0, l1 = shard(N, rank, world)
-    rows = ccm_fn(data, E, tau, Tp, mode, exclude_self, l0, l1)
-    full = gather_rows(rows, N, 0, group) if gather else None
+    rows_all = assign_rows(E, world, mode)
+    rows = ccm_fn(data, E, tau, Tp, mode, exclude_self, rows_all[rank])
+    full = gather_rows(rows, rows_all, N, 0, group) if gather else None
     return E, rows, full
 
 
@@ -96,25 +120,23 @@ def run_to_host(data: torch.Tensor, E_max: int, tau: int, Tp: int, mode, exclude
     N = data.shape[1]
     s0, s1 = shard(N, rank, world)
     E = all_gather_E(simplex_fn(data, E_max, tau, s0, s1), N, group)
+    rows_all = assign_rows(E, world, mode)
     cuda = data.is_cuda
     side = torch.cuda.Stream(device=data.device) if (cuda and rank == 0) else None
-    # chunk c of rank r: rows [b_r + c * step_r, ...) of its block [b_r, e_r)
-    # (chunks are whole multiples of the kernels' 256-library block, so none runs a partial block
-    # except at the end of a rank's rows)
-    blocks = [shard(N, r, world) for r in range(world)]
+    # chunk c of rank r: positions [c * step_r, (c + 1) * step_r) of its row list (chunks are whole
+    # multiples of the kernels' 256-library block, so none runs a partial block except at the end)
     def step_of(rows):
         want = -(-rows // nchunk)                   # ceil(rows / nchunk)
         return max(1, -(-want // align) * align)    # rounded up to a multiple of align
-    steps = [step_of(e - b) for b, e in blocks]
-    nchunk = max(-(-(e - b) // st) for (b, e), st in zip(blocks, steps))
+    steps = [step_of(len(r)) for r in rows_all]
+    nchunk = max(max(-(-len(r) // st) for r, st in zip(rows_all, steps)), 1)
     per = max(steps)
     bufs = None
     for c in range(nchunk):
-        b, e = blocks[rank]
-        r0, r1 = min(e, b + c * steps[rank]), min(e, b + (c + 1) * steps[rank])
+        mine = rows_all[rank][c * steps[rank]: (c + 1) * steps[rank]]
         buf = torch.empty((per, N), dtype=torch.float32, device=data.device)
-        if r1 > r0:
-            buf[: r1 - r0] = ccm_fn(data, E, tau, Tp, mode, exclude_self, r0, r1)
+        if mine.size:
+            buf[: mine.size] = ccm_fn(data, E, tau, Tp, mode, exclude_self, mine)
         if rank == 0:
             gl = [torch.empty_like(buf) for _ in range(world)]
             dist.gather(buf, gl, dst=0, group=group)
@@ -123,12 +145,15 @@ def run_to_host(data: torch.Tensor, E_max: int, tau: int, Tp: int, mode, exclude
             ctx = torch.cuda.stream(side) if side is not None else _nullctx()
             with ctx:
                 for r in range(world):
-                    rb, re = blocks[r]
-                    q0, q1 = min(re, rb + c * steps[r]), min(re, rb + (c + 1) * steps[r])
-                    if q1 > q0:
-                        rho_host[q0:q1].copy_(gl[r][: q1 - q0], non_blocking=side is not None)
+                    q = rows_all[r][c * steps[r]: (c + 1) * steps[r]]
+                    if not q.size:
+                        continue
+                    if _is_range(q):
+                        rho_host[int(q[0]): int(q[-1]) + 1].copy_(gl[r][: q.size], non_blocking=side is not None)
                         if side is not None:
                             gl[r].record_stream(side)
+                    else:  # dealt rows (library mode): scatter on the host
+                        rho_host[torch.from_numpy(q.astype(np.int64))] = gl[r][: q.size].cpu()
         else:
             dist.gather(buf, None, dst=0, group=group)
         bufs = buf  # keep the last local buffer alive until the collective has consumed it
@@ -153,8 +178,11 @@ def libccm_phase_fns():
     def simplex_fn(data, E_max, tau, s0, s1):
         return libccm.simplex_optimal_E(data, E_max, tau, s0, s1)
 
-    def ccm_fn(data, E, tau, Tp, mode, excl, l0, l1):
-        return libccm.ccm_all_pairs(data, E, tau, Tp, mode, excl, l0, l1)
+    def ccm_fn(data, E, tau, Tp, mode, excl, rows):
+        if _is_range(rows):  # contiguous block: the range call
+            l0 = int(rows[0]) if rows.size else 0
+            return libccm.ccm_all_pairs(data, E, tau, Tp, mode, excl, l0, l0 + int(rows.size))
+        return libccm.ccm_rows(data, E, rows, tau, Tp, mode, excl)
 
     return simplex_fn, ccm_fn
 

@@ -33,7 +33,7 @@ E_CAP = 20
 EXPORTS = ("edm_embed_knn", "edm_simplex_optimal_E", "edm_ccm_all_pairs", "edm_workspace_bytes",
            "edm_causal_map_host", "edm_last_error", "edm_version", "edm_profile_begin", "edm_profile_end",
            "edm_ccm_lagged", "edm_ccm_lagged_workspace_bytes", "edm_ccm_convergence",
-           "edm_ccm_convergence_workspace_bytes", "edm_ccm_tables", "edm_ccm_tables_workspace_bytes")
+           "edm_ccm_convergence_workspace_bytes", "edm_ccm_tables", "edm_ccm_tables_workspace_bytes", "edm_ccm_rows")
 PROF_KINDS = ("prep", "simplex_knn", "simplex_rho", "ccm_knn", "lookup", "other")
 
 
@@ -83,6 +83,8 @@ def load(path: Optional[str] = None):
                                         sz, vp]
     lib.edm_ccm_convergence_workspace_bytes.restype = sz
     lib.edm_ccm_convergence_workspace_bytes.argtypes = [i32, i32, i32, i32, i32, i32]
+    lib.edm_ccm_rows.restype = i32
+    lib.edm_ccm_rows.argtypes = [edm_dataset, vp, i32, i32, i32, i32, vp, i32, vp, vp, sz, vp]
     lib.edm_ccm_tables.restype = i32
     lib.edm_ccm_tables.argtypes = [edm_dataset, vp, i32, i32, i32, i32, i32, i32, vp, i32, i32, i32, vp, vp, vp, vp, sz,
                                    vp]
@@ -206,6 +208,26 @@ def ccm_all_pairs(data: torch.Tensor, E: torch.Tensor, tau: int = 1, Tp: int = 1
     ws = workspace(1, ds.N, ds.L, E_CAP, tau, Tp, data.device)
     _check(load().edm_ccm_all_pairs(ds, E.data_ptr(), tau, Tp, _mode(mode), int(exclude_self), lib_begin, lib_end,
                                     out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(data.device)))
+    return out
+
+
+def ccm_rows(data: torch.Tensor, E: torch.Tensor, lib_list, tau: int = 1, Tp: int = 1, mode="target",
+             exclude_self: bool = True, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Phase 2 for a list of library rows (edm_ccm_rows): rho[r, j] for library lib_list[r]."""
+    ds = _dataset(data)
+    _require_cuda(E, torch.int32, "E")
+    E = E.contiguous()
+    if E.numel() != ds.N:
+        raise ValueError("E must have N entries")
+    lst = np.ascontiguousarray(np.asarray(lib_list, dtype=np.int32).ravel())
+    rows = lst.size
+    if out is None:
+        out = torch.empty((rows, ds.N), dtype=torch.float32, device=data.device)
+    elif not out.is_contiguous() or out.numel() < rows * ds.N or out.dtype != torch.float32:
+        raise ValueError("out must be a contiguous float32 tensor with at least rows*N elements")
+    ws = workspace(1, ds.N, ds.L, E_CAP, tau, Tp, data.device)
+    _check(load().edm_ccm_rows(ds, E.data_ptr(), tau, Tp, _mode(mode), int(exclude_self), lst.ctypes.data if rows else None,
+                               rows, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(data.device)))
     return out
 
 

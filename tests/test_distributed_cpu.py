@@ -30,8 +30,10 @@ def _oracle_fns():
         e, _ = O.simplex_all(data.numpy(), E_max, tau, s0, s1, nthreads=1)
         return torch.from_numpy(e)
 
-    def ccm_fn(data, E, tau, Tp, mode, excl, l0, l1):
-        r = O.ccm_rows(data.numpy(), E.numpy(), tau, Tp, 0 if mode == "target" else 1, excl, l0, l1, nthreads=1)
+    def ccm_fn(data, E, tau, Tp, mode, excl, rows):
+        m = 0 if mode == "target" else 1
+        r = [O.ccm_rows(data.numpy(), E.numpy(), tau, Tp, m, excl, int(i), int(i) + 1, nthreads=1) for i in rows]
+        r = np.concatenate(r) if r else np.zeros((0, data.shape[1]))
         return torch.from_numpy(r.astype(np.float32))
 
     return simplex_fn, ccm_fn
@@ -73,6 +75,22 @@ def test_shard_covers_everything():
             assert all(parts[i][1] == parts[i + 1][0] for i in range(w - 1))
             sizes = [b - a for a, b in parts]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_assign_rows_partitions_and_balances():
+    rng = np.random.default_rng(4)
+    E = rng.integers(1, 21, 1001).astype(np.int32)
+    for mode in ("target", "library"):
+        for w in (1, 2, 3, 8):
+            parts = D.assign_rows(E, w, mode)
+            allrows = np.sort(np.concatenate(parts))
+            assert np.array_equal(allrows, np.arange(1001))
+            assert all(np.all(np.diff(p) > 0) for p in parts)
+            if mode == "target":
+                assert all(D._is_range(p) for p in parts)
+            else:  # E-sorted dealing: per-rank sums of E within one max E of each other
+                sums = [int(E[p].sum()) for p in parts]
+                assert max(sums) - min(sums) <= 20
 
 
 @pytest.mark.parametrize("world,mode", [(2, "target"), (3, "library")])

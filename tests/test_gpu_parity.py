@@ -293,3 +293,25 @@ def test_lagged_c3_shape_sampled_and_causal_lag():
     pair = delayed_pair(1000, 3)
     r = libccm.ccm_lagged(dev(pair), dev(np.array([2, 2]), torch.int32), 1, -6, 3).cpu().numpy()
     assert -6 + int(np.argmax(r[1, :, 0])) == -4
+
+
+# ---------------------------------------------------------------- edm_ccm_rows (library lists, multi-GPU dealing)
+def test_ccm_rows_list_equals_range_rows():
+    """A library LIST gives exactly the rows of the range call (byte for byte), in list order,
+    duplicates included; library mode deals rows this way across GPUs."""
+    data = synth.make_config("c2", N=300, L=400)
+    d = dev(data)
+    E = libccm.simplex_optimal_E(d, 20)
+    rng = np.random.default_rng(8)
+    lst = np.concatenate([rng.permutation(300)[:270], [5, 5, 299]]).astype(np.int32)
+    for mode in ("target", "library"):
+        full = libccm.ccm_all_pairs(d, E, 1, 1, mode).cpu().numpy()
+        rows = libccm.ccm_rows(d, E, lst, 1, 1, mode).cpu().numpy()
+        assert np.array_equal(rows.view(np.uint32), full[lst].view(np.uint32))
+    Eh = E.cpu().numpy()
+    from paper_2011_11082_b200 import distributed as D
+    parts = D.assign_rows(Eh, 3, "library")
+    got = np.concatenate([libccm.ccm_rows(d, E, p, 1, 1, "library").cpu().numpy() for p in parts])
+    order = np.concatenate(parts)
+    full = libccm.ccm_all_pairs(d, E, 1, 1, "library").cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), full[order].view(np.uint32))
