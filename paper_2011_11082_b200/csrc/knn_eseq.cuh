@@ -29,23 +29,40 @@ constexpr int ESQ_SORT = 2048;     // capacity of the per-CTA sort of the candid
 __host__ __device__ constexpr int esq_loff(int e) { return e * (e + 5) / 2; }  // list of E = e+1: e+3 labels
 constexpr int ESQ_LAB = esq_loff(ECAP);  // 250
 
+#ifdef CCM_ESQ_STATS
+// debug build only (-DCCM_ESQ_STATS): per-E counters [E][0 flagged, 1 rounds, 2 S2 seeds, 3 S1 seeds,
+// 4 fillers, 5 theta inf, 6 (query, E) count]
+__device__ unsigned long long esq_stats[ECAP + 1][8];
+#define ESQ_STAT(E, i, v) do { const unsigned long long v_ = (v); if (lane == 0) atomicAdd(&esq_stats[E][i], v_); } while (0)
+#else
+#define ESQ_STAT(E, i, v) do { } while (0)
+#endif
+
+constexpr int ESQ_BUF = 128;       // flagged candidates compacted per (query, E); more -> rounds
+constexpr int ESQ_QPW_MAX = 63;    // run length limit of the 11-bit (query, E) stamps
 struct EsqWarp {
     int lab[ESQ_LAB];       // per E: labels of the last finished list (K = E+2 entries, -1 = none)
     double sD[ECAP + 4];    // the list being selected: exact keys, sorted, K <= 22 entries
     int sS[ECAP + 4];
+    float fbuf[ESQ_BUF];          // compacted fp32 sweep values of the flagged candidates
+    unsigned short buf[ESQ_BUF];  // compacted labels of the flagged candidates
+    unsigned short tag[ESQ_SORT]; // per candidate label: (stamp << 5 | entry) if it is an S2 seed now
 };
 
 // shared memory: [xs: padl + 32 NC + PADR floats][slab: ESQ_SORT u16][pos: ESQ_SORT u16]
 //                [union: sort keys ESQ_SORT u64 | ESQ_WARPS EsqWarp]
-// the whole series (phase 1 reads queries from its second half) and every register chunk's candidates
+// left padding (even, so that element 0 of the series is 8-byte aligned for paired loads)
+__host__ __device__ constexpr int esq_padl(int tau) { return (knn_padl(tau) + 1) & ~1; }
+// one staged copy: the whole series (phase 1 reads queries from its second half) and every register
+// chunk's candidates; two copies are kept, the second shifted by one sample (paired loads at odd offsets)
 __host__ __device__ constexpr size_t esq_xs_floats(int tau, int NC, int L) {
-    return (size_t)knn_padl(tau) + (L > 32 * NC ? L : 32 * NC) + KNN_PADR;
+    return ((size_t)esq_padl(tau) + (L > 32 * NC ? L : 32 * NC) + KNN_PADR + 3) & ~(size_t)3;
 }
 __host__ __device__ constexpr size_t esq_union_bytes() {
     return (size_t)ESQ_SORT * 8 > ESQ_WARPS * sizeof(EsqWarp) ? (size_t)ESQ_SORT * 8 : ESQ_WARPS * sizeof(EsqWarp);
 }
 __host__ __device__ constexpr size_t esq_smem_bytes(int tau, int NC, int L) {
-    return (esq_xs_floats(tau, NC, L) * 4 + 15) / 16 * 16 + 2 * ESQ_SORT * 2 + esq_union_bytes();
+    return 2 * esq_xs_floats(tau, NC, L) * 4 + 2 * ESQ_SORT * 2 + esq_union_bytes();
 }
 
 __device__ __forceinline__ unsigned f32_order(float v) {
@@ -57,6 +74,17 @@ __device__ __forceinline__ float esq_upper(float v) { return __fadd_ru(__fmaf_ru
 // fp32 sweep threshold admitting every candidate whose exact distance is <= theta
 __device__ __forceinline__ float esq_thresh(float theta) {
     return fminf(THR_EMPTY, __fadd_ru(__fmaf_ru(theta, 0x1p-18f, theta), 0x1p-140f));
+}
+
+// packed fp32 pairs (FADD2 / FFMA2 on sm_100a): two candidates per instruction in the sweep
+__device__ __forceinline__ unsigned long long f2_bits(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
+__device__ __forceinline__ float2 bits_f2(unsigned long long u) { return *reinterpret_cast<float2*>(&u); }
+// D + (q - v)^2 per component, each rounded exactly as fmaf(q - v, q - v, D)
+__device__ __forceinline__ float2 sq_acc2(unsigned long long q2, float2 v, float2 D) {
+    unsigned long long d, r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(q2), "l"(f2_bits(v)));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(d), "l"(f2_bits(D)));
+    return bits_f2(r);
 }
 
 // exact fp64 D_E(t, s), the oracle's C3 operation sequence (separately rounded sub, mul, add)
@@ -100,10 +128,76 @@ __device__ __forceinline__ int esq_merge(EsqWarp& W, int cnt, int K, bool act, d
     return min(cnt + __popc(am), K);
 }
 
+// (D, s) order of C4: ascending distance, lowest label on exact ties
+__device__ __forceinline__ bool key_less(double a, int sa, double b, int sb) { return a < b || (a == b && sa < sb); }
+// one compare-exchange stage of a warp bitonic network (partner lane ^ j; `up` = ascending block)
+__device__ __forceinline__ void bitonic_step(double& D, int& S, int j, bool up, int lane) {
+    const double oD = __shfl_xor_sync(FULL, D, j);
+    const int oS = __shfl_xor_sync(FULL, S, j);
+    const bool lower = (lane & j) == 0;
+    const bool oLess = key_less(oD, oS, D, S);
+    if (lower == up ? oLess : !oLess) { D = oD; S = oS; }
+}
+// sort the warp's 32 (D, S) keys ascending by lane (keys are distinct: S differ)
+__device__ __forceinline__ void warp_sort(double& D, int& S, int lane) {
+#pragma unroll
+    for (int k2 = 2; k2 <= 32; k2 <<= 1)
+#pragma unroll
+        for (int j = k2 >> 1; j > 0; j >>= 1) bitonic_step(D, S, j, (lane & k2) == 0 || k2 == 32, lane);
+}
+// sort a bitonic sequence of 32 keys ascending
+__device__ __forceinline__ void warp_merge(double& D, int& S, int lane) {
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) bitonic_step(D, S, j, true, lane);
+}
+
+// candidate label of flag bit b of a lane (pairs s = 2l + 64c + h, b = 2c + h)
+__device__ __forceinline__ int esq_label(int lane, int b) { return 2 * lane + 32 * (b & ~1) + (b & 1); }
+
+// fp32 D_E(t, s) exactly as the sweep forms it (fmaf(q - x, q - x, D) for m = 0..E-1)
+__device__ __forceinline__ float esq_f32(const float* __restrict__ qaf, const float* __restrict__ cbf, int t, int s,
+                                         int E, int tau) {
+    float v = 0.f;
+    for (int m = 0; m < E; ++m) {
+        const float d = qaf[t - m * tau] - cbf[s - m * tau];
+        v = fmaf(d, d, v);
+    }
+    return v;
+}
+
+// warp bitonic network on 64-bit keys (fp32 value bits << 32 | label): non-negative floats order as
+// their bits, labels break exact value ties (those are near ties for the certification anyway).
+// One compare-exchange stage: partner lane ^ j, `up` = ascending block.
+__device__ __forceinline__ void bitonic_step_u64(unsigned long long& K, int j, bool up, int lane) {
+    const unsigned long long o = __shfl_xor_sync(FULL, K, j);
+    const bool lower = (lane & j) == 0;
+    const bool oLess = o < K;
+    if (lower == up ? oLess : !oLess) K = o;
+}
+// sort the first n (power of two <= 32) lanes ascending (other lanes sort among themselves);
+// loops, not unrolled: the kernel is large and instruction-cache misses cost more than loop control
+__device__ __forceinline__ void warp_sort_u64(unsigned long long& K, int n, int lane) {
+#pragma unroll 1
+    for (int k2 = 2; k2 <= n; k2 <<= 1)
+#pragma unroll 1
+        for (int j = k2 >> 1; j > 0; j >>= 1) bitonic_step_u64(K, j, (lane & k2) == 0 || k2 == n, lane);
+}
+__device__ __forceinline__ void warp_merge_u64(unsigned long long& K, int lane) {
+#pragma unroll 1
+    for (int j = 16; j > 0; j >>= 1) bitonic_step_u64(K, j, true, lane);
+}
+__device__ __forceinline__ unsigned long long fkey(unsigned v, int s) { return ((unsigned long long)v << 32) | (unsigned)s; }
+// the fp32 order of two sorted sweep values a <= b is the exact order of their fp64 keys when
+// they are separated by more than both error bands (|D~ - D| <= 2^-18 D + 2^-140, see header)
+__device__ __forceinline__ bool fp32_separated(float a, float b) {
+    return __fsub_rd(b, a) > __fadd_ru(__fmul_ru(__fadd_ru(a, b), 0x1p-17f), 0x1p-138f);
+}
+
 // One warp, queries t_begin .. t_end-1 in order (see the file header). NC = register chunks.
 template <int MODE, bool TAU1, int NC>
 __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const float* __restrict__ qaf,
-                                         const float* __restrict__ cbf, const unsigned short* __restrict__ slab,
+                                         const float* __restrict__ cbf, const float* __restrict__ cbf1,
+                                         const unsigned short* __restrict__ slab,
                                          const unsigned short* __restrict__ pos, int t_begin, int t_end, int ncand,
                                          int Etop, int b, int lane, double unscale) {
     const int tau = TAU1 ? 1 : P.tau;
@@ -111,11 +205,13 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
     int prevEq = 0;  // lab[] holds the lists of query t-1 for E <= prevEq
     for (int t = t_begin; t < t_end; ++t) {
         const int Eq = min(Etop, t / tau + 1);
-        float D[NC];
+        // lane l owns the candidate pairs s = 2l + 64c + {0, 1}; flag bit b <-> esq_label(lane, b)
+        float2 D[NC / 2];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            const int s = lane + 32 * c;
-            D[c] = (s < ncand && !(excl && s == t)) ? 0.f : CUDART_INF_F;
+        for (int c = 0; c < NC / 2; ++c) {
+            const int s = 2 * lane + 64 * c;
+            D[c].x = (s < ncand && !(excl && s == t)) ? 0.f : CUDART_INF_F;
+            D[c].y = (s + 1 < ncand && !(excl && s + 1 == t)) ? 0.f : CUDART_INF_F;
         }
         // position of x[t] among the sorted candidate values (E = 1 seeds)
         const float q0 = qaf[t];
@@ -140,171 +236,244 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
         } else {
             p = pos[t];
         }
-        // S2 seeds: this query's list at E-1, lane j = entry j (exact D_{E-1}, label)
-        double curD = CUDART_INF;
+        // carried pool: this query's selection at E-1, lane j = entry j (fp32 sweep value, label),
+        // sorted; it seeds the threshold at E
+        float curF = CUDART_INF_F;
         int curS = -1, cntPrev = 0;
         for (int e = 0; e < Eq; ++e) {
             const int E = e + 1, k = E + 1, K = E + 2;
             const float qe = qaf[t - e * tau];
-            // ---------------- 1. threshold from the seeds
-            float uA = CUDART_INF_F, uB = CUDART_INF_F;
-            bool aOn = false, bOn = false;
-            int sA = -1, sB = -1;
+            const unsigned stamp = (unsigned)(((t - t_begin) << 5) | e) + 1u;  // unique per (query, E) in the run
+            // ---------------- 1. threshold from the seeds. Seed bounds U >= 0 are handled as
+            // order-preserving integer keys (float bits + 1; 0 = no seed) for hardware warp max (REDUX)
+            unsigned kA = 0u, kB = 0u;
             if (e == 0) {
                 const int i = p - 3 + lane;
                 if (lane < 7 && i >= 0 && i < ncand) {
                     const int s = slab[i];
                     if (!(excl && s == t)) {
                         const float d = q0 - cbf[s];
-                        uA = esq_upper(fmaf(d, d, 0.f));
-                        aOn = true;
-                        sA = s;
+                        kA = __float_as_uint(esq_upper(fmaf(d, d, 0.f))) + 1u;
                     }
                 }
-            } else {
-                if (lane < cntPrev && curS - e * tau >= 0) {
-                    const double diff = __dsub_rn((double)qe, (double)cbf[curS - e * tau]);
-                    curD = __dadd_rn(curD, __dmul_rn(diff, diff));  // exact D_E of list entry `lane`
-                    uA = __double2float_ru(curD);
-                    aOn = true;
-                    sA = curS;
-                }
-                if (e < prevEq && lane < K) {
-                    const int l = W.lab[esq_loff(e) + lane];
-                    const int s = l + 1;
-                    if (l >= 0 && s < ncand && s - e * tau >= 0 && !(excl && s == t)) {
-                        float v = 0.f;
-                        for (int m = 0; m <= e; ++m) {
-                            const float d = qaf[t - m * tau] - cbf[s - m * tau];
-                            v = fmaf(d, d, v);
-                        }
-                        uB = esq_upper(v);
-                        bOn = true;
-                        sB = s;
-                    }
+            } else if (lane < cntPrev && curS - e * tau >= 0) {
+                const float d = qe - cbf[curS - e * tau];
+                curF = fmaf(d, d, curF);  // the sweep's own fp32 value of entry `lane` at E
+                if (lane < K) kA = __float_as_uint(esq_upper(curF)) + 1u;  // the K best as seeds
+                W.tag[curS] = (unsigned short)((stamp << 5) | (unsigned)lane);
+            }
+            __syncwarp();
+            const int nA = __popc(__ballot_sync(FULL, kA != 0u));
+            // the k-th smallest of >= k carried seeds is at most their max; S1 seeds at or above it
+            // cannot lower the k-th smallest of the union and are dropped
+            const unsigned thA = nA >= k ? __reduce_max_sync(FULL, kA) : 0xffffffffu;
+            if (e > 0 && e < prevEq && lane < K) {
+                const int l = W.lab[esq_loff(e) + lane];
+                const int s = l + 1;
+                if (l >= 0 && s < ncand && s - e * tau >= 0 && !(excl && s == t) &&
+                    (W.tag[s] >> 5) != stamp) {  // not already a carried seed
+                    const float u = esq_upper(esq_f32(qaf, cbf, t, s, E, tau));
+                    const unsigned kv = __float_as_uint(u) + 1u;
+                    if (kv < thA) kB = kv;
                 }
             }
-            const unsigned amask = __ballot_sync(FULL, aOn);
+            // theta = k-th smallest seed bound = the max after removing the (U - k) largest of the
+            // U seeds (usually U - k = the few S1 seeds below the carried bound)
+            const int U = nA + __popc(__ballot_sync(FULL, kB != 0u));
             float theta = CUDART_INF_F;
-            {
-                // S1 seeds at or above the S2 bound cannot lower the k-th smallest: drop them
-                float mA = aOn ? uA : 0.f;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) mA = fmaxf(mA, __shfl_xor_sync(FULL, mA, o));
-                const int nA = __popc(amask);
-                if (nA >= k) bOn = bOn && uB < mA;  // the k-th smallest of the union is <= mA
-                // rank of every seed value in the union (ties: S2 before S1, then lane); duplicate
-                // labels (an S1 seed already in S2) are dropped while S2 is broadcast
-                int rA = 0, rB = 0;
-                bool dup = false;
-                for (unsigned m = amask; m; m &= m - 1) {
-                    const int j = __ffs(m) - 1;
-                    const float v = __shfl_sync(FULL, uA, j);
-                    const int sj = __shfl_sync(FULL, sA, j);
-                    rA += (v < uA || (v == uA && j < lane)) ? 1 : 0;
-                    rB += (v <= uB) ? 1 : 0;
-                    dup = dup || (sj == sB);
-                }
-                bOn = bOn && !dup;
-                const unsigned bmask = __ballot_sync(FULL, bOn);
-                if (!bmask && nA == k) {
-                    theta = mA;  // exactly k S2 seeds and no S1 seed below them: their max
-                } else {
-                    for (unsigned m = bmask; m; m &= m - 1) {
-                        const int j = __ffs(m) - 1;
-                        const float v = __shfl_sync(FULL, uB, j);
-                        rA += (v < uA) ? 1 : 0;
-                        rB += (v < uB || (v == uB && j < lane)) ? 1 : 0;
+            if (U >= k) {
+                for (int i = 0; i < U - k; ++i) {
+                    const unsigned M = __reduce_max_sync(FULL, max(kA, kB));
+                    const int h = __ffs(__ballot_sync(FULL, kA == M || kB == M)) - 1;
+                    if (lane == h) {
+                        if (kA == M) kA = 0u;
+                        else kB = 0u;
                     }
-                    const bool hit = (aOn && rA == k - 1) || (bOn && rB == k - 1);
-                    const unsigned hm = __ballot_sync(FULL, hit);
-                    if (hm) theta = __shfl_sync(FULL, (aOn && rA == k - 1) ? uA : uB, __ffs(hm) - 1);
                 }
+                theta = __uint_as_float(__reduce_max_sync(FULL, max(kA, kB)) - 1u);
             }
             const float T = esq_thresh(theta);
+            ESQ_STAT(E, 2, nA);
+            ESQ_STAT(E, 3, U - nA);
+            ESQ_STAT(E, 5, theta == CUDART_INF_F ? 1 : 0);
+            ESQ_STAT(E, 6, 1);
             // ---------------- 2. sweep: update the register distances to E, flag D <= T
             unsigned pm0 = 0u, pm1 = 0u;
-            const float* cs = cbf + lane - e * tau;
+            {
+                // pairs (x[o], x[o+1]), o = 2l + 64c - e tau: 8-byte aligned in the original copy for
+                // even o, in the copy shifted by one sample (cbf1[j] = x[j+1]) for odd o
+                const int off = 2 * lane - e * tau;
+                const float* base = (off & 1) ? cbf1 + off - 1 : cbf + off;
+                const unsigned long long q2 = f2_bits(make_float2(qe, qe));
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                const float d = qe - cs[32 * c];
-                D[c] = fmaf(d, d, D[c]);
-                if (D[c] <= T) {
-                    if (c < 32) pm0 |= 1u << c;
-                    else pm1 |= 1u << (c - 32);
+                for (int c = 0; c < NC / 2; ++c) {
+                    D[c] = sq_acc2(q2, *reinterpret_cast<const float2*>(base + 64 * c), D[c]);
+                    if (D[c].x <= T) {
+                        if (2 * c < 32) pm0 |= 1u << (2 * c);
+                        else pm1 |= 1u << (2 * c - 32);
+                    }
+                    if (D[c].y <= T) {
+                        if (2 * c + 1 < 32) pm0 |= 1u << (2 * c + 1);
+                        else pm1 |= 1u << (2 * c + 1 - 32);
+                    }
                 }
             }
-            // ---------------- 3. exact selection of the flagged candidates (rounds of <= 32)
+            // ---------------- 3. selection of the flagged candidates: compacted with their fp32 sweep
+            // values and sorted by (value, label) across the warp; the order is certified exact when
+            // every adjacent pair up to position k is separated beyond the fp32 error bands, else
+            // the (query, E) is re-sorted on exact fp64 keys
+            unsigned kv = 0xffffffffu;  // lane i = i-th smallest: fp32 value bits ...
+            int ks = 0x40000000 + lane;   // ... and label (sentinels sort after every real entry)
+            double exD = CUDART_INF;      // exact key of lane i (only after an exact re-sort)
+            bool exact = false;
             int cnt = 0;
-            while (__any_sync(FULL, (pm0 | pm1) != 0u)) {
-                const bool act = (pm0 | pm1) != 0u;
-                int s = 0;
-                double Dx = CUDART_INF;
-                if (act) {
-                    int c;
-                    if (pm0) { c = __ffs(pm0) - 1; pm0 &= pm0 - 1; }
-                    else { c = 32 + __ffs(pm1) - 1; pm1 &= pm1 - 1; }
-                    s = lane + 32 * c;
-                    Dx = esq_exact(qaf, cbf, t, s, E, tau);
+            {
+                const int mine = __popc(pm0) + __popc(pm1);
+                int pre = mine;  // inclusive prefix over the lanes
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(FULL, pre, o);
+                    if (lane >= o) pre += v;
                 }
-                if (cnt == 0) {
-                    const unsigned am = __ballot_sync(FULL, act);
-                    int rank = 0;
-                    for (unsigned m = am; m; m &= m - 1) {
-                        const int j = __ffs(m) - 1;
-                        const double Dj = __shfl_sync(FULL, Dx, j);
-                        const int sj = __shfl_sync(FULL, s, j);
-                        rank += (Dj < Dx || (Dj == Dx && sj < s)) ? 1 : 0;
+                const int m = __shfl_sync(FULL, pre, 31);
+                ESQ_STAT(E, 0, m);
+                if (m <= ESQ_BUF) {
+                    for (int w = pre - mine; pm0 | pm1; ++w) {
+                        int bb;
+                        if (pm0) { bb = __ffs(pm0) - 1; pm0 &= pm0 - 1; }
+                        else { bb = 32 + __ffs(pm1) - 1; pm1 &= pm1 - 1; }
+                        W.buf[w] = (unsigned short)esq_label(lane, bb);
                     }
                     __syncwarp();
-                    if (act && rank < K) { W.sD[rank] = Dx; W.sS[rank] = s; }
+                    for (int b0 = 0; b0 < m; b0 += 32) {
+                        ESQ_STAT(E, 1, 1);
+                        unsigned long long bk = ~0ull - lane;
+                        if (b0 + lane < m) {
+                            const int s = W.buf[b0 + lane];
+                            bk = fkey(__float_as_uint(esq_f32(qaf, cbf, t, s, E, tau)), s);
+                        }
+                        if (b0 == 0) {
+                            int n2 = 2;
+                            while (n2 < m && n2 < 32) n2 <<= 1;
+                            warp_sort_u64(bk, n2, lane);
+                            kv = (unsigned)(bk >> 32);
+                            ks = (int)(bk & 0xffffffffu);
+                        } else {  // keep the 32 smallest of two sorted runs, then re-sort (bitonic merge)
+                            warp_sort_u64(bk, 32, lane);
+                            const unsigned long long r = __shfl_sync(FULL, bk, 31 - lane);
+                            unsigned long long cur = fkey(kv, ks);
+                            if (r < cur) cur = r;
+                            warp_merge_u64(cur, lane);
+                            kv = (unsigned)(cur >> 32);
+                            ks = (int)(cur & 0xffffffffu);
+                        }
+                    }
+                    cnt = min(m, 32);
+                    // certification of positions 0..k (the table's order and the set boundary)
+                    const float f = __uint_as_float(kv);
+                    const float fn = __shfl_down_sync(FULL, f, 1);
+                    const bool tie = lane < k && lane + 1 < cnt && !fp32_separated(f, fn);
+                    exact = __any_sync(FULL, tie);
                     __syncwarp();
-                    cnt = min(__popc(am), K);
-                } else {
-                    cnt = esq_merge(W, cnt, K, act, Dx, s, lane);
+                }
+                if (m > ESQ_BUF || exact) {
+                    // exact fp64 keys of every flagged candidate (near ties of the fp32 order, exact
+                    // ties of quantised data, tie floods): merged with the exact pre-test
+                    ESQ_STAT(E, 7, 1);
+                    if (m > ESQ_BUF) {  // re-flag (the compaction buffer was too small)
+                        pm0 = pm1 = 0u;
+#pragma unroll
+                        for (int c = 0; c < NC / 2; ++c) {
+                            if (D[c].x <= T) { if (2 * c < 32) pm0 |= 1u << (2 * c); else pm1 |= 1u << (2 * c - 32); }
+                            if (D[c].y <= T) { if (2 * c + 1 < 32) pm0 |= 1u << (2 * c + 1); else pm1 |= 1u << (2 * c + 1 - 32); }
+                        }
+                    }
+                    int ecnt = 0;
+                    for (int b0 = 0; (m > ESQ_BUF) ? __any_sync(FULL, (pm0 | pm1) != 0u) : b0 < m; b0 += 32) {
+                        bool act;
+                        int s = 0;
+                        if (m > ESQ_BUF) {
+                            act = (pm0 | pm1) != 0u;
+                            if (act) {
+                                int bb;
+                                if (pm0) { bb = __ffs(pm0) - 1; pm0 &= pm0 - 1; }
+                                else { bb = 32 + __ffs(pm1) - 1; pm1 &= pm1 - 1; }
+                                s = esq_label(lane, bb);
+                            }
+                        } else {
+                            act = b0 + lane < m;
+                            if (act) s = W.buf[b0 + lane];
+                        }
+                        const double Dx = act ? esq_exact(qaf, cbf, t, s, E, tau) : CUDART_INF;
+                        ecnt = esq_merge(W, ecnt, K, act, Dx, s, lane);
+                    }
+                    cnt = ecnt;
+                    if (lane < cnt) {
+                        exD = W.sD[lane];
+                        ks = W.sS[lane];
+                        kv = __float_as_uint(esq_f32(qaf, cbf, t, ks, E, tau));  // the carried fp32 value
+                    } else {
+                        kv = 0xffffffffu;
+                        ks = 0x40000000 + lane;
+                    }
+                    exact = true;
+                    __syncwarp();
                 }
             }
             const int nsel = cnt;  // >= k whenever the threshold is sound
-            // fewer than K flagged (tight threshold): complete the carried list with the lowest
-            // valid labels not in it, so that the seeds at E+1 still bound the k-th distance
+            // fewer than K (tight threshold): complete the carried set with the lowest valid labels
+            // not in it, so that the seeds at E+1 can still bound the k-th distance
             if (cnt < K) {
                 const int lo = E * tau;  // valid at E+1 as well
-                int sf = lo + lane;
+                const int sf = lo + lane;
                 bool ok = sf < ncand && !(excl && sf == t);
-                for (int j = 0; j < cnt; ++j) ok = ok && (W.sS[j] != sf);
-                const unsigned okm = __ballot_sync(FULL, ok);
-                const int pre = __popc(okm & ((1u << lane) - 1u));
-                __syncwarp();
-                if (ok && cnt + pre < K) {
-                    W.sD[cnt + pre] = esq_exact(qaf, cbf, t, sf, E, tau);
-                    W.sS[cnt + pre] = sf;
+                for (int j = 0; j < cnt; ++j) {
+                    const int sj = __shfl_sync(FULL, ks, j);  // every lane
+                    ok = ok && sj != sf;
                 }
+                const unsigned okm = __ballot_sync(FULL, ok);
+                const int rank = cnt + __popc(okm & ((1u << lane) - 1u));  // destination lane
+                const float fv = (ok && rank < K) ? esq_f32(qaf, cbf, t, sf, E, tau) : CUDART_INF_F;
+                __syncwarp();
+                if (ok && rank < K) { W.fbuf[rank] = fv; W.buf[rank] = (unsigned short)sf; }
                 __syncwarp();
                 const int add = min(__popc(okm), K - cnt);
+                if (lane >= cnt && lane < cnt + add) { kv = __float_as_uint(W.fbuf[lane]); ks = W.buf[lane]; }
+                __syncwarp();
+                ESQ_STAT(E, 4, add);
                 // the fillers only serve as seeds: the table uses the first k entries, which the
                 // flagged candidates fill whenever the threshold is sound (k <= flagged)
                 cnt += add;
             }
-            // ---------------- 4. finalise E: table / lists, carry the list as the S2 seeds of E+1
-            double d2 = lane < cnt ? W.sD[lane] : CUDART_INF;
-            int sl = lane < cnt ? W.sS[lane] : -1;
-            __syncwarp();
+            // ---------------- 4. finalise E: table, lists; the sorted set is the carried pool of E+1
+            const float fsel = __uint_as_float(kv);
+            int sl = lane < cnt ? ks : -1;
             if (lane < K) W.lab[esq_loff(e) + lane] = sl;
-            curD = d2;
+            curF = lane < cnt ? fsel : CUDART_INF_F;
             curS = sl;
             cntPrev = cnt;
             const int row = t - e * tau;
             // never store a sentinel (see knn_warp): entries the selection did not fill -> NaN rows
-            const bool unfilled = lane < k && (lane >= nsel || !(d2 < CUDART_INF));
-            if (unfilled) { sl = t; d2 = CUDART_NAN; }
+            const bool unfilled = lane < k && lane >= nsel;
+            if (unfilled) sl = t;
             const bool any_unfilled = __any_sync(FULL, unfilled);
+            // exact squared distance where it is stored (phase-1 lists; the table readback)
+            const bool need_exact = MODE == MODE_SIMPLEX || (MODE == MODE_CCM && P.tdist);
+            double d2 = CUDART_INF;
+            if (need_exact && lane < k && !unfilled) d2 = exact ? exD : esq_exact(qaf, cbf, t, sl, E, tau);
             if (MODE == MODE_CCM) {
+                // S8 fused: weights of C5 from the fp32 sweep distances (relative error
+                // < 2^-18: weights within 1e-6); ratios d_j/d_1 are invariant under the sweep rescaling
                 const int kp = kpad(k);
                 float wv;
-                if (__any_sync(FULL, lane < k && d2 < 0x1p-100)) {
-                    wv = (float)simplex_weight<false>(d2, k, lane);
+                const float fk = lane < k ? fsel : 0.f;
+                if (__any_sync(FULL, lane < k && fk < 0x1p-100f)) {
+                    // tiny distances: the exact keys and fp64 ratios
+                    const double dx = (lane < k && !unfilled) ? (exact ? exD : esq_exact(qaf, cbf, t, sl, E, tau))
+                                                              : CUDART_INF;
+                    wv = (float)simplex_weight<false>(dx, k, lane);
                 } else {
-                    const float df = lane < k ? __fsqrt_rn(__double2float_rn(d2)) : 0.f;
+                    const float df = lane < k ? __fsqrt_rn(fk) : 0.f;
                     const float d1 = __shfl_sync(FULL, df, 0);
                     float u = d1 > 0.f ? __expf(-__fdividef(df, d1)) : (df == 0.f ? 1.f : 0.f);
                     u = lane < k ? fmaxf(u, 1e-6f) : 0.f;
@@ -318,12 +487,12 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
                     const int64_t o = (int64_t)b * P.T_lib + P.offE[E] + (int64_t)row * kp + lane;
                     P.tables[o] = lane < k ? make_uint2((unsigned)(sl + P.store_shift), __float_as_uint(wv))
                                            : make_uint2(0u, 0u);
-                    if (P.tdist) P.tdist[o] = lane < k ? (float)(sqrt(d2) * unscale) : 0.f;
+                    if (P.tdist) P.tdist[o] = lane < k ? (any_unfilled ? CUDART_NAN_F : (float)(sqrt(d2) * unscale)) : 0.f;
                 }
-            } else {  // MODE_SIMPLEX: the (d2, s) list goes to forecast_kernel (ratios only: scale-free)
+            } else {  // MODE_SIMPLEX: the exact (d2, s) list goes to forecast_kernel (ratios only: scale-free)
                 if (lane < k) {
                     const int64_t o = (int64_t)b * P.S_slot + P.offS[E] + (int64_t)t * k + lane;
-                    P.sd2[o] = d2;
+                    P.sd2[o] = any_unfilled ? CUDART_NAN : d2;
                     P.ss[o] = sl;
                 }
             }
@@ -342,21 +511,26 @@ __global__ void __launch_bounds__(ESQ_WARPS * 32, KNN_MIN_CTAS) knn_eseq_kernel(
     const int b = blockIdx.y;
     const int row = P.slot_series ? P.slot_series[b] : b;
     const float* xg = P.X + (int64_t)row * P.ldx;
-    const int padl = knn_padl(P.tau);
+    const int padl = esq_padl(P.tau);
     const int nx = (int)esq_xs_floats(P.tau, NC, P.L);
     const int kexp = P.sexp ? P.sexp[row] : P.sexp0;
     const double unscale = ldexp(1.0, -kexp), sc = ldexp(1.0, kexp);
     float* xs = reinterpret_cast<float*>(esq_smem);
-    unsigned short* slab = reinterpret_cast<unsigned short*>(esq_smem + (esq_xs_floats(P.tau, NC, P.L) * 4 + 15) / 16 * 16);
+    float* xs1 = xs + nx;  // the same padded series shifted by one sample
+    unsigned short* slab = reinterpret_cast<unsigned short*>(xs1 + nx);
     unsigned short* pos = slab + ESQ_SORT;
     unsigned char* un = reinterpret_cast<unsigned char*>(pos + ESQ_SORT);
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+    for (int i = threadIdx.x; i < nx + 1; i += blockDim.x) {
         const int t = i - padl;
-        xs[i] = (t >= 0 && t < P.L) ? (kexp ? (float)((double)xg[t] * sc) : xg[t]) : 1e30f;
+        const float v = (t >= 0 && t < P.L) ? (kexp ? (float)((double)xg[t] * sc) : xg[t]) : 1e30f;
+        if (i < nx) xs[i] = v;
+        if (i >= 1) xs1[i - 1] = v;
     }
     const float* xf = xs + padl;
+    const float* xf1 = xs1 + padl;
     const float* qaf;
     const float* cbf;
+    const float* cbf1 = xf1;
     int nq, ncand;
     if (MODE == MODE_SIMPLEX) {
         const int Llib = (P.L + 1) / 2;  // library = first ceil(L/2) samples
@@ -397,10 +571,12 @@ __global__ void __launch_bounds__(ESQ_WARPS * 32, KNN_MIN_CTAS) knn_eseq_kernel(
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     EsqWarp& W = reinterpret_cast<EsqWarp*>(un)[warp];
+    for (int i = lane; i < ESQ_SORT; i += 32) W.tag[i] = 0;  // no stamp (stamps start at 1)
+    __syncwarp();
     const int qpw = P.qpw > 0 ? P.qpw : KNN_QPW;
     const int t0 = (blockIdx.x * ESQ_WARPS + warp) * qpw;
     const int t1 = min(nq, t0 + qpw);
-    if (t0 < t1) esq_warp<MODE, TAU1, NC>(P, W, qaf, cbf, slab, pos, t0, t1, ncand, P.Etop, b, lane, unscale);
+    if (t0 < t1) esq_warp<MODE, TAU1, NC>(P, W, qaf, cbf, cbf1, slab, pos, t0, t1, ncand, P.Etop, b, lane, unscale);
 }
 
 }  // namespace ccm

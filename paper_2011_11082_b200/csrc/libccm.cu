@@ -315,7 +315,7 @@ edm_status launch_knn(const KnnParams& P0, int nq, int slots, cudaStream_t st) {
         const int ncand = MODE == MODE_SIMPLEX ? (P.L + 1) / 2 - 1 : P.L - P.Tp;
         if (esq_eligible<MODE>(P, full, ncand)) {
             const char* qenv = getenv("CCM_ESQ_QPW");
-            const int qmax = qenv ? std::max(1, atoi(qenv)) : CCM_ESQ_QPW;
+            const int qmax = std::min(ESQ_QPW_MAX, qenv ? std::max(1, atoi(qenv)) : CCM_ESQ_QPW);
             const int nc = std::max(1, (nq + ESQ_WARPS * qmax - 1) / (ESQ_WARPS * qmax));
             P.qpw = std::max(1, (nq + nc * ESQ_WARPS - 1) / (nc * ESQ_WARPS));
             dim3 g((nq + ESQ_WARPS * P.qpw - 1) / (ESQ_WARPS * P.qpw), slots);
@@ -438,6 +438,16 @@ edm_status edm_profile_end(double* ms, int64_t* launches) {
     g_prof.used = 0;
     return EDM_OK;
 }
+
+#ifdef CCM_ESQ_STATS
+// debug build only: copy out and reset the E-sequential kNN counters ([21][8] uint64)
+edm_status edm_debug_esq_stats(unsigned long long* out) {
+    CUDA_TRY(cudaMemcpyFromSymbol(out, esq_stats, sizeof(esq_stats)));
+    static unsigned long long zero[ECAP + 1][8] = {};
+    CUDA_TRY(cudaMemcpyToSymbol(esq_stats, zero, sizeof(zero)));
+    return EDM_OK;
+}
+#endif
 
 const char* edm_version(void) { return "libccm 0.1 sm_100a (fp64 exact kNN, fp32 lookup)"; }
 
