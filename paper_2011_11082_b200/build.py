@@ -14,6 +14,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "lib", "libccm.so")
+LIB_CHECKED = os.path.join(PKG, "lib", "libccm_checked.so")  # -DCCM_CHECKS: device bounds checks
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -29,25 +30,28 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h"))
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or _stale():
-        tmp = f"{LIB}.tmp{os.getpid()}"  # per process: concurrent ranks never write the same file
-        cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", tmp, *sources()]
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    lib = LIB_CHECKED if checked else LIB
+    if force or _stale(lib):
+        tmp = f"{lib}.tmp{os.getpid()}"  # per process: concurrent ranks never write the same file
+        cmd = ["nvcc", *NVCC_FLAGS, *(["-DCCM_CHECKS"] if checked else []), "-I", INCLUDE, "-I", CSRC, "-o", tmp,
+               *sources()]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
-        os.makedirs(os.path.dirname(LIB), exist_ok=True)
+        os.makedirs(os.path.dirname(lib), exist_ok=True)
         subprocess.check_call(cmd)
-        os.replace(tmp, LIB)  # atomic
-    return LIB
+        os.replace(tmp, lib)  # atomic
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import sys
+    print(build(force=True, verbose=True, checked="--checked" in sys.argv))

@@ -17,6 +17,23 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+// Checked builds (-DCCM_CHECKS, build.py --checked -> lib/libccm_checked.so): device-side bounds
+// and invariant checks on the kernels' indexed shared/global accesses, which trap with the failing
+// line (compute-sanitizer is not available on the GPU pool; tests/test_gpu_checked.py runs every
+// kernel variant under this build instead).
+#ifdef CCM_CHECKS
+#include <cstdio>
+#define CCM_CHECK(c)                                                                     \
+    do {                                                                                 \
+        if (!(c)) {                                                                      \
+            printf("CCM_CHECK failed: %s at %s:%d\n", #c, __FILE__, __LINE__);          \
+            __trap();                                                                    \
+        }                                                                                \
+    } while (0)
+#else
+#define CCM_CHECK(c) do { } while (0)
+#endif
+
 namespace ccm {
 
 constexpr int ECAP = 20;            // largest E (k = E + 1 <= 21 <= 32 lanes)
@@ -552,6 +569,7 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
             }
             const int nU = min(KNN_UMAX, tot0 + __shfl_sync(FULL, off1, 31));
             off1 += tot0 - cnt1;
+            CCM_CHECK(mw == 0 || ncand <= mw);
             for (unsigned w = w0; w; w &= w - 1, ++off)
                 if (off < KNN_UMAX) W.ulist[off] = (lane << 5) + __ffs(w) - 1;
             for (unsigned w = w1; w; w &= w - 1, ++off1)
@@ -606,6 +624,8 @@ __device__ __forceinline__ void knn_warp(const KnnParams& P, KnnWarpSmem& W, uns
                 if (any_unfilled) wv = CUDART_NAN_F;
                 if (lane < kp) {
                     const int64_t o = (int64_t)b * P.T_lib + P.offE[e + 1] + (int64_t)row * kp + lane;
+                    CCM_CHECK(o >= 0 && o < (int64_t)gridDim.y * P.T_lib && P.offE[e + 1] + (int64_t)(row + 1) * kp <= P.T_lib);
+                    CCM_CHECK(lane >= k || (sl >= 0 && sl < P.L));
                     P.tables[o] = lane < k ? make_uint2((unsigned)(sl + P.store_shift), __float_as_uint(wv))
                                            : make_uint2(0u, 0u);
                     if (P.tdist) P.tdist[o] = lane < k ? (float)(sqrt(d2) * unscale) : 0.f;
@@ -916,11 +936,14 @@ __device__ __forceinline__ void lookup_one(const LookupParams& P, const float* _
 #pragma unroll
             for (int j2 = 0; j2 < kp / 2; ++j2) {
                 const uint4 e2 = row[j2];
+                CCM_CHECK((int)e2.x + P.gshift >= 0 && (int)e2.x + P.gshift < P.Lt);
+                CCM_CHECK(2 * j2 + 1 >= k || ((int)e2.z + P.gshift >= 0 && (int)e2.z + P.gshift < P.Lt));
                 p = fmaf(__uint_as_float(e2.y), Yl(e2.x), p);
                 if (2 * j2 + 1 < k) p = fmaf(__uint_as_float(e2.w), Yl(e2.z), p);
             }
             if (r == 0) c = p;
             p -= c;
+            CCM_CHECK(t0 + P.oshift + r >= 0 && t0 + P.oshift + r < P.Lt);
             const float o = Yo[(int64_t)r * ys];
             sp += p;
             spp = fmaf(p, p, spp);

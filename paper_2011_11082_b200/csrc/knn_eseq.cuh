@@ -90,6 +90,7 @@ __device__ __forceinline__ float2 sq_acc2(unsigned long long q2, float2 v, float
 // exact fp64 D_E(t, s), the oracle's C3 operation sequence (separately rounded sub, mul, add)
 __device__ __forceinline__ double esq_exact(const float* __restrict__ qaf, const float* __restrict__ cbf, int t, int s,
                                             int E, int tau) {
+    CCM_CHECK(s >= (E - 1) * tau && t >= (E - 1) * tau);
     double D = 0.0;
     for (int m = 0; m < E; ++m) {
         const double diff = __dsub_rn((double)qaf[t - m * tau], (double)cbf[s - m * tau]);
@@ -101,6 +102,7 @@ __device__ __forceinline__ double esq_exact(const float* __restrict__ qaf, const
 // Merge the active lanes' candidates (exact key (Dx, s)) into the sorted list sD/sS of cnt
 // entries (capacity K); ties -> lower label (C4). Returns the new count.
 __device__ __forceinline__ int esq_merge(EsqWarp& W, int cnt, int K, bool act, double Dx, int s, int lane) {
+    CCM_CHECK(cnt <= K && K <= ECAP + 2);
     if (cnt == K) {  // exact pre-test against the K-th key (cuts tie floods, e.g. a constant series)
         const double thD = W.sD[K - 1];
         const int thS = W.sS[K - 1];
@@ -157,6 +159,7 @@ __device__ __forceinline__ int esq_label(int lane, int b) { return 2 * lane + 32
 // fp32 D_E(t, s) exactly as the sweep forms it (fmaf(q - x, q - x, D) for m = 0..E-1)
 __device__ __forceinline__ float esq_f32(const float* __restrict__ qaf, const float* __restrict__ cbf, int t, int s,
                                          int E, int tau) {
+    CCM_CHECK(s >= (E - 1) * tau && t >= (E - 1) * tau);
     float v = 0.f;
     for (int m = 0; m < E; ++m) {
         const float d = qaf[t - m * tau] - cbf[s - m * tau];
@@ -260,6 +263,7 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
                 const float d = qe - cbf[curS - e * tau];
                 curF = fmaf(d, d, curF);  // the sweep's own fp32 value of entry `lane` at E
                 if (lane < K) kA = __float_as_uint(esq_upper(curF)) + 1u;  // the K best as seeds
+                CCM_CHECK(curS >= 0 && curS < ncand && stamp < 2048u);
                 W.tag[curS] = (unsigned short)((stamp << 5) | (unsigned)lane);
             }
             __syncwarp();
@@ -342,6 +346,7 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
                         int bb;
                         if (pm0) { bb = __ffs(pm0) - 1; pm0 &= pm0 - 1; }
                         else { bb = 32 + __ffs(pm1) - 1; pm1 &= pm1 - 1; }
+                        CCM_CHECK(w < ESQ_BUF && esq_label(lane, bb) < ncand);
                         W.buf[w] = (unsigned short)esq_label(lane, bb);
                     }
                     __syncwarp();
@@ -448,6 +453,7 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
             // ---------------- 4. finalise E: table, lists; the sorted set is the carried pool of E+1
             const float fsel = __uint_as_float(kv);
             int sl = lane < cnt ? ks : -1;
+            CCM_CHECK(lane >= K || (esq_loff(e) + lane < ESQ_LAB && (sl == -1 || (sl >= e * tau && sl < ncand))));
             if (lane < K) W.lab[esq_loff(e) + lane] = sl;
             curF = lane < cnt ? fsel : CUDART_INF_F;
             curS = sl;
@@ -485,6 +491,8 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
                 if (any_unfilled) wv = CUDART_NAN_F;
                 if (lane < kp) {
                     const int64_t o = (int64_t)b * P.T_lib + P.offE[E] + (int64_t)row * kp + lane;
+                    CCM_CHECK(o >= 0 && o < (int64_t)gridDim.y * P.T_lib && P.offE[E] + (int64_t)(row + 1) * kp <= P.T_lib);
+                    CCM_CHECK(lane >= k || (sl >= e * tau && sl < ncand));
                     P.tables[o] = lane < k ? make_uint2((unsigned)(sl + P.store_shift), __float_as_uint(wv))
                                            : make_uint2(0u, 0u);
                     if (P.tdist) P.tdist[o] = lane < k ? (any_unfilled ? CUDART_NAN_F : (float)(sqrt(d2) * unscale)) : 0.f;
@@ -562,8 +570,10 @@ __global__ void __launch_bounds__(ESQ_WARPS * 32, KNN_MIN_CTAS) knn_eseq_kernel(
                 __syncthreads();
             }
         }
+        CCM_CHECK(P2 <= ESQ_SORT);
         for (int i = threadIdx.x; i < ncand; i += blockDim.x) {
             const int l = (int)(keys[i] & 0xffffffffu);
+            CCM_CHECK(l >= 0 && l < ncand);
             slab[i] = (unsigned short)l;
             pos[l] = (unsigned short)i;
         }

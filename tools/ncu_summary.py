@@ -33,6 +33,11 @@ KEYS = [
     ("launch__block_size", "block"),
     ("lts__t_bytes.sum", "l2_bytes"),
     ("sm__cycles_elapsed.avg", "sm_cycles"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "fp32_fma_pipe_pct"),
+    ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", "fmaheavy_pipe_pct"),
+    ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "alu_pipe_pct"),
+    ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "lsu_inst_pct"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "xu_inst_pct"),
 ]
 
 
@@ -90,8 +95,17 @@ def full(rep, out_path, traffic_path=None, kernel=None):
     with open(out_path, "w") as f:
         f.write("\n".join(lines) + "\n")
     if traffic_path and traffic:
+        try:
+            with open(traffic_path) as f:
+                old = json.load(f)
+        except Exception:
+            old = {}
+        old.update({k: v for k, v in traffic.items() if k.endswith("_per_launch")})
+        old.setdefault("sources", {})[kernel] = {"report": traffic["source"], "kernel": traffic["kernel"]}
+        old.pop("source", None)
+        old.pop("kernel", None)
         with open(traffic_path, "w") as f:
-            json.dump(traffic, f, indent=1)
+            json.dump(old, f, indent=1)
     print("\n".join(lines))
 
 
