@@ -210,8 +210,9 @@ def test_sugihara_direction_on_gpu():
 # ---------------------------------------------------------------- full BASELINE size, sampled
 def test_c3_full_size_sampled():
     """c3 at full size (53,053 x 1,450, the bench workload) in the bench's launch
-    configuration (64-library blocks, all targets): optE bit-exact on sampled series, rho
-    within 1e-4 on every target of sampled library rows (the oracle computes them one by one)."""
+    configuration (whole 256-library blocks, all targets): optE bit-exact on sampled series (all
+    series: tests/test_gpu_full_optE.py), rho within 1e-4 on every target of sampled library rows
+    (the oracle computes them one by one)."""
     data = synth.make_config("c3")
     L, N = data.shape
     d = dev(data)
@@ -222,9 +223,9 @@ def test_c3_full_size_sampled():
         e, _, _ = O.simplex(data[:, s].astype(np.float64), 20)
         assert e == optE[s], (s, e, optE[s])
     E_dev = dev(optE, torch.int32)
-    for r0 in (0, 26496, N - 64):
-        rows = libccm.ccm_all_pairs(d, E_dev, 1, 1, "target", True, r0, r0 + 64).cpu().numpy()
-        pick = [0, 17, 63]
+    for r0 in (0, 26368, N - 256):
+        rows = libccm.ccm_all_pairs(d, E_dev, 1, 1, "target", True, r0, r0 + 256).cpu().numpy()
+        pick = [0, 117, 255]
         ref = np.concatenate([O.ccm_rows(data, optE, 1, 1, 0, True, r0 + p, r0 + p + 1) for p in pick])
         assert_rho_close(rows[pick], ref)
 

@@ -89,7 +89,7 @@ def full(rep, out_path, traffic_path=None, kernel=None):
                     pass
         stalls.sort(reverse=True)
         lines.append("  top stalls (warps per issue): " + ", ".join(f"{n}={v:.2f}" for v, n in stalls[:6]))
-        if kernel and kernel in name and "dram_read_B" in vals:
+        if kernel and (kernel in name or (kernel == "ccm_knn" and "knn" in name)) and "dram_read_B" in vals:
             traffic = {f"{kernel}_dram_bytes_per_launch": vals["dram_read_B"] + vals.get("dram_write_B", 0.0),
                        "source": rep, "kernel": name}
     with open(out_path, "w") as f:
