@@ -38,6 +38,9 @@ __device__ unsigned long long esq_stats[ECAP + 1][8];
 #define ESQ_STAT(E, i, v) do { } while (0)
 #endif
 
+#ifndef CCM_ESQ_RANKSORT
+#define CCM_ESQ_RANKSORT 0
+#endif
 constexpr int ESQ_BUF = 128;       // flagged candidates compacted per (query, E); more -> rounds
 constexpr int ESQ_QPW_MAX = 63;    // run length limit of the 11-bit (query, E) stamps
 struct EsqWarp {
@@ -45,6 +48,7 @@ struct EsqWarp {
     double sD[ECAP + 4];    // the list being selected: exact keys, sorted, K <= 22 entries
     int sS[ECAP + 4];
     float fbuf[ESQ_BUF];          // compacted fp32 sweep values of the flagged candidates
+    unsigned long long rkey[32];  // rank-sort scatter buffer
     unsigned short buf[ESQ_BUF];  // compacted labels of the flagged candidates
     unsigned short tag[ESQ_SORT]; // per candidate label: (stamp << 5 | entry) if it is an S2 seed now
 };
@@ -167,6 +171,31 @@ __device__ __forceinline__ float esq_f32(const float* __restrict__ qaf, const fl
     }
     return v;
 }
+// (x[j], x[j+1]) as one aligned 8-byte load: from x for even j, from the shifted copy x1
+// (x1[i] = x[i+1]) for odd j
+__device__ __forceinline__ float2 ld_pair(const float* __restrict__ x, const float* __restrict__ x1, int j) {
+    return *reinterpret_cast<const float2*>((j & 1) ? x1 + j - 1 : x + j);
+}
+// tau = 1: the same value as esq_f32 (identical operation sequence), two terms per pair of loads.
+// x / x1: the staged series and its shifted copy; the query is x[qo + t], the candidate x[s].
+__device__ __forceinline__ float esq_f32_t1(const float* __restrict__ x, const float* __restrict__ x1, int qo, int t,
+                                            int s, int E) {
+    CCM_CHECK(s >= E - 1 && t >= E - 1);
+    float v = 0.f;
+    int m = 0;
+    for (; m + 1 < E; m += 2) {
+        const float2 q = ld_pair(x, x1, qo + t - m - 1), c = ld_pair(x, x1, s - m - 1);
+        const float d0 = q.y - c.y;  // term m: x[t - m] - x[s - m]
+        v = fmaf(d0, d0, v);
+        const float d1 = q.x - c.x;  // term m + 1
+        v = fmaf(d1, d1, v);
+    }
+    if (m < E) {
+        const float d = x[qo + t - m] - x[s - m];
+        v = fmaf(d, d, v);
+    }
+    return v;
+}
 
 // warp bitonic network on 64-bit keys (fp32 value bits << 32 | label): non-negative floats order as
 // their bits, labels break exact value ties (those are near ties for the certification anyway).
@@ -205,6 +234,11 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
                                          int Etop, int b, int lane, double unscale) {
     const int tau = TAU1 ? 1 : P.tau;
     const bool excl = (MODE != MODE_SIMPLEX) && P.excl;
+    const int qo = (int)(qaf - cbf);  // offset of the query half (phase 1) in the staged series
+    // fp32 distance of candidate s exactly as the sweep forms it
+    auto f32 = [&](int t_, int s_, int E_) {
+        return TAU1 ? esq_f32_t1(cbf, cbf1, qo, t_, s_, E_) : esq_f32(qaf, cbf, t_, s_, E_, tau);
+    };
     int prevEq = 0;  // lab[] holds the lists of query t-1 for E <= prevEq
     for (int t = t_begin; t < t_end; ++t) {
         const int Eq = min(Etop, t / tau + 1);
@@ -276,7 +310,7 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
                 const int s = l + 1;
                 if (l >= 0 && s < ncand && s - e * tau >= 0 && !(excl && s == t) &&
                     (W.tag[s] >> 5) != stamp) {  // not already a carried seed
-                    const float u = esq_upper(esq_f32(qaf, cbf, t, s, E, tau));
+                    const float u = esq_upper(f32(t, s, E));
                     const unsigned kv = __float_as_uint(u) + 1u;
                     if (kv < thA) kB = kv;
                 }
@@ -355,12 +389,26 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
                         unsigned long long bk = ~0ull - lane;
                         if (b0 + lane < m) {
                             const int s = W.buf[b0 + lane];
-                            bk = fkey(__float_as_uint(esq_f32(qaf, cbf, t, s, E, tau)), s);
+                            bk = fkey(__float_as_uint(f32(t, s, E)), s);
                         }
                         if (b0 == 0) {
+#if CCM_ESQ_RANKSORT
+                            // rank by counting (m <= 32 comparisons per lane), then scatter/gather
+                            const int mm = min(m, 32);
+                            int rank = 0;
+                            for (int j = 0; j < mm; ++j) {
+                                const unsigned long long o = __shfl_sync(FULL, bk, j);
+                                rank += (o < bk) ? 1 : 0;
+                            }
+                            __syncwarp();
+                            if (lane < mm) W.rkey[rank] = bk;
+                            __syncwarp();
+                            bk = lane < mm ? W.rkey[lane] : ~0ull - lane;
+#else
                             int n2 = 2;
                             while (n2 < m && n2 < 32) n2 <<= 1;
                             warp_sort_u64(bk, n2, lane);
+#endif
                             kv = (unsigned)(bk >> 32);
                             ks = (int)(bk & 0xffffffffu);
                         } else {  // keep the 32 smallest of two sorted runs, then re-sort (bitonic merge)
@@ -416,7 +464,7 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
                     if (lane < cnt) {
                         exD = W.sD[lane];
                         ks = W.sS[lane];
-                        kv = __float_as_uint(esq_f32(qaf, cbf, t, ks, E, tau));  // the carried fp32 value
+                        kv = __float_as_uint(f32(t, ks, E));  // the carried fp32 value
                     } else {
                         kv = 0xffffffffu;
                         ks = 0x40000000 + lane;
@@ -438,7 +486,7 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
                 }
                 const unsigned okm = __ballot_sync(FULL, ok);
                 const int rank = cnt + __popc(okm & ((1u << lane) - 1u));  // destination lane
-                const float fv = (ok && rank < K) ? esq_f32(qaf, cbf, t, sf, E, tau) : CUDART_INF_F;
+                const float fv = (ok && rank < K) ? f32(t, sf, E) : CUDART_INF_F;
                 __syncwarp();
                 if (ok && rank < K) { W.fbuf[rank] = fv; W.buf[rank] = (unsigned short)sf; }
                 __syncwarp();
