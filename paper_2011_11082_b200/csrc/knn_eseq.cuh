@@ -25,7 +25,8 @@ namespace ccm {
 
 constexpr int ESQ_WARPS = 4;
 constexpr int ESQ_NCMAX = 48;      // candidate chunks per lane held in registers (ncand <= 1536)
-constexpr int ESQ_SORT = 2048;     // capacity of the per-CTA sort of the candidate values
+constexpr int ESQ_SORT = 2048;     // capacity of the per-CTA sort of the candidate values (a power of two)
+constexpr int ESQ_CAND = 32 * ESQ_NCMAX;  // candidates per series (sorted labels, positions, stamps)
 __host__ __device__ constexpr int esq_loff(int e) { return e * (e + 5) / 2; }  // list of E = e+1: e+3 labels
 constexpr int ESQ_LAB = esq_loff(ECAP);  // 250
 
@@ -39,7 +40,10 @@ __device__ unsigned long long esq_stats[ECAP + 1][8];
 #endif
 
 #ifndef CCM_ESQ_RANKSORT
-#define CCM_ESQ_RANKSORT 0
+#define CCM_ESQ_RANKSORT 1   // rank-count sort of the first batch (else the bitonic network): -1.5 % / -5 %
+#endif
+#ifndef CCM_ESQ_PAIRF32
+#define CCM_ESQ_PAIRF32 0    // paired 8-byte loads in the fp32 recompute (tau = 1)
 #endif
 constexpr int ESQ_BUF = 128;       // flagged candidates compacted per (query, E); more -> rounds
 constexpr int ESQ_QPW_MAX = 63;    // run length limit of the 11-bit (query, E) stamps
@@ -47,13 +51,15 @@ struct EsqWarp {
     int lab[ESQ_LAB];       // per E: labels of the last finished list (K = E+2 entries, -1 = none)
     double sD[ECAP + 4];    // the list being selected: exact keys, sorted, K <= 22 entries
     int sS[ECAP + 4];
-    float fbuf[ESQ_BUF];          // compacted fp32 sweep values of the flagged candidates
-    unsigned long long rkey[32];  // rank-sort scatter buffer
+    union {
+        float fbuf[ESQ_BUF];          // fp32 values of the filler candidates
+        unsigned long long rkey[32];  // rank-sort scatter buffer
+    };
     unsigned short buf[ESQ_BUF];  // compacted labels of the flagged candidates
-    unsigned short tag[ESQ_SORT]; // per candidate label: (stamp << 5 | entry) if it is an S2 seed now
+    unsigned short tag[ESQ_CAND]; // per candidate label: (stamp << 5 | entry) if it is a carried seed now
 };
 
-// shared memory: [xs: padl + 32 NC + PADR floats][slab: ESQ_SORT u16][pos: ESQ_SORT u16]
+// shared memory: [xs, xs1: two padded copies][slab: ESQ_CAND u16][pos: ESQ_CAND u16]
 //                [union: sort keys ESQ_SORT u64 | ESQ_WARPS EsqWarp]
 // left padding (even, so that element 0 of the series is 8-byte aligned for paired loads)
 __host__ __device__ constexpr int esq_padl(int tau) { return (knn_padl(tau) + 1) & ~1; }
@@ -66,7 +72,7 @@ __host__ __device__ constexpr size_t esq_union_bytes() {
     return (size_t)ESQ_SORT * 8 > ESQ_WARPS * sizeof(EsqWarp) ? (size_t)ESQ_SORT * 8 : ESQ_WARPS * sizeof(EsqWarp);
 }
 __host__ __device__ constexpr size_t esq_smem_bytes(int tau, int NC, int L) {
-    return 2 * esq_xs_floats(tau, NC, L) * 4 + 2 * ESQ_SORT * 2 + esq_union_bytes();
+    return 2 * esq_xs_floats(tau, NC, L) * 4 + 2 * ESQ_CAND * 2 + esq_union_bytes();
 }
 
 __device__ __forceinline__ unsigned f32_order(float v) {
@@ -237,7 +243,7 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
     const int qo = (int)(qaf - cbf);  // offset of the query half (phase 1) in the staged series
     // fp32 distance of candidate s exactly as the sweep forms it
     auto f32 = [&](int t_, int s_, int E_) {
-        return TAU1 ? esq_f32_t1(cbf, cbf1, qo, t_, s_, E_) : esq_f32(qaf, cbf, t_, s_, E_, tau);
+        return (TAU1 && CCM_ESQ_PAIRF32) ? esq_f32_t1(cbf, cbf1, qo, t_, s_, E_) : esq_f32(qaf, cbf, t_, s_, E_, tau);
     };
     int prevEq = 0;  // lab[] holds the lists of query t-1 for E <= prevEq
     for (int t = t_begin; t < t_end; ++t) {
@@ -574,8 +580,8 @@ __global__ void __launch_bounds__(ESQ_WARPS * 32, KNN_MIN_CTAS) knn_eseq_kernel(
     float* xs = reinterpret_cast<float*>(esq_smem);
     float* xs1 = xs + nx;  // the same padded series shifted by one sample
     unsigned short* slab = reinterpret_cast<unsigned short*>(xs1 + nx);
-    unsigned short* pos = slab + ESQ_SORT;
-    unsigned char* un = reinterpret_cast<unsigned char*>(pos + ESQ_SORT);
+    unsigned short* pos = slab + ESQ_CAND;
+    unsigned char* un = reinterpret_cast<unsigned char*>(pos + ESQ_CAND);
     for (int i = threadIdx.x; i < nx + 1; i += blockDim.x) {
         const int t = i - padl;
         const float v = (t >= 0 && t < P.L) ? (kexp ? (float)((double)xg[t] * sc) : xg[t]) : 1e30f;
@@ -629,7 +635,7 @@ __global__ void __launch_bounds__(ESQ_WARPS * 32, KNN_MIN_CTAS) knn_eseq_kernel(
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     EsqWarp& W = reinterpret_cast<EsqWarp*>(un)[warp];
-    for (int i = lane; i < ESQ_SORT; i += 32) W.tag[i] = 0;  // no stamp (stamps start at 1)
+    for (int i = lane; i < ESQ_CAND; i += 32) W.tag[i] = 0;  // no stamp (stamps start at 1)
     __syncwarp();
     const int qpw = P.qpw > 0 ? P.qpw : KNN_QPW;
     const int t0 = (blockIdx.x * ESQ_WARPS + warp) * qpw;
