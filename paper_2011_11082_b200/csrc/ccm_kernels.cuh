@@ -985,7 +985,8 @@ __device__ __forceinline__ void lookup_dispatch(int E, const LookupParams& P, co
     }
 }
 
-constexpr size_t lookup_ring_bytes() { return (size_t)LOOKUP_WARPS * LK_STAGES * (LK_CHUNK + 8); }
+// per-warp rings + their mbarriers + the tile barrier (16 B)
+constexpr size_t lookup_ring_bytes() { return (size_t)LOOKUP_WARPS * LK_STAGES * (LK_CHUNK + 8) + 16; }
 
 // grid = ntiles; block = LOOKUP_WARPS * 32. SMEM = true: the 32-column target tile
 // tile block (yp_index: [L][32] contiguous) is staged in shared memory once and reused by
@@ -1029,8 +1030,21 @@ __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupPara
     int64_t ys;
     const float* src = P.Yp + yp_index(tile * TILE_J, 0, P.Lt);  // the tile's contiguous [L][32] block
     if (SMEM) {
-        for (int i = threadIdx.x; i < P.Lt * (TILE_J / 4); i += blockDim.x)
-            reinterpret_cast<float4*>(ytile)[i] = __ldg(reinterpret_cast<const float4*>(src) + i);
+        // the tile's contiguous [L][32] block staged by TMA bulk copies (cp.async.bulk, 32 KB each)
+        // completing on one mbarrier; every thread waits on its phase 0
+        uint64_t* tbar = bars + LOOKUP_WARPS * LK_STAGES;
+        const uint32_t total = (uint32_t)P.Lt * TILE_J * sizeof(float);
+        constexpr uint32_t TCH = 32768;
+        if (threadIdx.x == 0) {
+            mbar_init(tbar, (total + TCH - 1) / TCH);
+            fence_mbar_init();
+            fence_proxy_async();
+            for (uint32_t off = 0; off < total; off += TCH)
+                tma_load_1d(reinterpret_cast<char*>(ytile) + off, reinterpret_cast<const char*>(src) + off,
+                            min(TCH, total - off), tbar);
+        }
+        __syncthreads();  // the barrier's initialisation is visible before anyone waits on it
+        mbar_wait(tbar, 0u);
         Y = ytile;
     } else {
         Y = src;  // gathers from L2/HBM; byte offsets idx * 128 + lane * 4 stay 32-bit (L < 2^25)
