@@ -124,19 +124,6 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t *E, int32_t tau, int3
                              int32_t lib_end, float *rho, void *workspace, size_t ws_bytes,
                              void *stream);
 
-/* edm_ccm_all_pairs with options. flags:
- *   EDM_LOOKUP_FP16 -- the lookup reads the targets as fp16 (centred, each scaled by a power of two
- *     so that max |y - mean| lies in (1/2, 1], then rounded to fp16): 64-target tiles, one half2
- *     gather per neighbour for two targets, so each table broadcast serves twice as many targets.
- *     Reduced precision: rho within 1e-4 of the fp64 oracle is tested (fp16 rounding of the
- *     targets moves rho by ~1e-5), NOT the headline configuration. Requires the target tile in
- *     shared memory (L up to about 1,800; else EUNSUPPORTED). kNN tables are unchanged (bit-exact).
- * Same workspace and errors as edm_ccm_all_pairs; unknown flags are EINVAL. */
-#define EDM_LOOKUP_FP16 1u
-edm_status edm_ccm_all_pairs_ex(edm_dataset ds, const int32_t *E, int32_t tau, int32_t Tp, edm_e_mode mode,
-                                int32_t exclude_self, int32_t lib_begin, int32_t lib_end, uint32_t flags, float *rho,
-                                void *workspace, size_t ws_bytes, void *stream);
-
 /* Phase 2 for an arbitrary LIST of library rows (the same computation as edm_ccm_all_pairs; used to
  * deal library rows to GPUs by E in library mode, where a library's cost grows with its own E,
  * SURVEY 8(e)): rho[r * N + j] = skill of cross-mapping series j from series lib_list[r].

@@ -13,7 +13,6 @@
 //   argmax_kernel         optE = argmax_E rho(E)                                (S3)
 //   lookup_kernel<TILE>   gather-weighted lookup + fused Pearson moments        (S9)
 #pragma once
-#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
@@ -105,7 +104,7 @@ __host__ __device__ __forceinline__ int sweep_exponent(float mx) {
 // lookup's fp32 moments; Pearson rho is scale-invariant), else 0.
 __global__ void scan_kernel(const float* __restrict__ y, int64_t ld, int c0, int n, int L,
                             int* __restrict__ sexp, double* __restrict__ mean, int* __restrict__ texp,
-                            int* __restrict__ bad, int* __restrict__ hexp = nullptr) {
+                            int* __restrict__ bad) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     const float* col = y + c0 + j;
@@ -145,11 +144,6 @@ __global__ void scan_kernel(const float* __restrict__ y, int64_t ld, int c0, int
         int e = 0;
         if (mc > 0.0) { (void)frexp(mc, &e); --e; }
         texp[j] = (mc > 0.0 && (e >= 30 || e < -30)) ? -e : 0;
-        if (hexp) {  // fp16 lookup: max |y - mean| 2^hexp in (1/2, 1]
-            int eh = 0;
-            if (mc > 0.0) (void)frexp(mc, &eh);  // mc in [2^(eh-1), 2^eh)
-            hexp[j] = mc > 0.0 ? -eh : 0;
-        }
     }
 }
 
@@ -172,37 +166,14 @@ __global__ void permute_kernel(const float* __restrict__ y, int64_t ld, int L, i
         Yp[yp_index(p, t, L)] = c >= 0 ? (float)(((double)y[(int64_t)t * ld + c] - mu) * sc) : 0.f;
 }
 
-// fp16-target variant of the lookup (EDM_LOOKUP_FP16, not the headline): 64-target tiles, lane l
-// of a warp holding targets 2l and 2l+1 as one half2. Element (p, t) is component p & 1 of half2
-// Yh2[yh_index(p, t, L)]; every target is centred and scaled by 2^hexp so that max |y - mean| lies
-// in (1/2, 1] (fp16's range; rho is scale-invariant), then rounded to fp16.
-constexpr int TILE_H = 64;
-__host__ __device__ __forceinline__ int64_t yh_index(int p, int t, int L) {
-    return ((int64_t)(p >> 6) * L + t) * 32 + ((p & 63) >> 1);
-}
-__global__ void permute_half_kernel(const float* __restrict__ y, int64_t ld, int L, int Np,
-                                    const int* __restrict__ colmap, const double* __restrict__ mean,
-                                    const int* __restrict__ hexp, __half* __restrict__ Yh) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= Np) return;
-    const int c = colmap[p];
-    const double mu = c >= 0 ? mean[c] : 0.0;
-    const double sc = c >= 0 ? ldexp(1.0, hexp[c]) : 1.0;
-    for (int t = blockIdx.y; t < L; t += gridDim.y)
-        Yh[yh_index(p, t, L) * 2 + (p & 1)] =
-            __float2half_rn(c >= 0 ? (float)(((double)y[(int64_t)t * ld + c] - mu) * sc) : 0.f);
-}
-
 // Observed-window statistics for every E: the observation of table row r
 // at E is y[(E-1)tau + d + r], r < n_E, i.e. the window [(E-1)tau + d, obs_end] (obs_end is
 // the same for every E). stats[(E-1)*Np + p] = (sum y, sum y^2) of the centred fp32 column
 // over it (fp64), cflag[(E-1)*Np + p] = 1 if every raw value in it is equal (NaN skill).
 // Single-horizon CCM: d = Tp, obs_end = L-1; time-delay cross map: d = m_lo + lag.
-// With Yh (the fp16 variant) the sums are over the fp16 targets the lookup observes.
 __global__ void stats_kernel(const float* __restrict__ Yp, int L, const float* __restrict__ y, int64_t ld,
                              const int* __restrict__ colmap, int Np, int tau, int d, int obs_end, int Emax,
-                             double2* __restrict__ stats, int* __restrict__ cflag,
-                             const __half* __restrict__ Yh = nullptr) {
+                             double2* __restrict__ stats, int* __restrict__ cflag) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= Np) return;
     const int c = colmap[p];
@@ -215,7 +186,7 @@ __global__ void stats_kernel(const float* __restrict__ Yp, int L, const float* _
         cflag[(int64_t)(e - 1) * Np + p] = 1;
     }
     for (int t = obs_end; t >= 0 && e >= 1; --t) {
-        const double v = Yh ? (double)__half2float(Yh[yh_index(p, t, L) * 2 + (p & 1)]) : (double)Yp[yp_index(p, t, L)];
+        const double v = (double)Yp[yp_index(p, t, L)];
         s1 += v;
         s2 += v * v;
         if (c >= 0 && y[(int64_t)t * ld + c] != last) same = false;
@@ -1015,109 +986,6 @@ __device__ __forceinline__ void lookup_dispatch(int E, const LookupParams& P, co
 }
 
 // per-warp rings + their mbarriers + the tile barrier (16 B)
-// fp16-target lookup (EDM_LOOKUP_FP16): lane l predicts targets 2l, 2l+1 of a 64-target tile from
-// one half2 gather per neighbour; the table broadcast is shared by 64 targets instead of 32, so a
-// row costs k gathers + k/2 table broadcasts + 1 observation for 64 targets. Arithmetic as in
-// lookup_one, on the fp16-rounded targets (rho within 1e-4 of the fp64 oracle, tested).
-__device__ __forceinline__ float2 f2fma(float w, float2 y, float2 a) {
-    unsigned long long r;
-    const float2 w2 = make_float2(w, w);
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(*reinterpret_cast<const unsigned long long*>(&w2)),
-        "l"(*reinterpret_cast<const unsigned long long*>(&y)), "l"(*reinterpret_cast<const unsigned long long*>(&a)));
-    return *reinterpret_cast<float2*>(&r);
-}
-template <int E>
-__device__ __forceinline__ void lookup_one_h(const LookupParams& P, const __half2* __restrict__ Y, int tile, int b,
-                                             int lane, int col0, int col1, WarpRing& R) {
-    constexpr int k = E + 1, kp = kpad(k);
-    constexpr int ROWS = LK_CHUNK / (8 * kp);
-    constexpr int CB = ROWS * kp * 8;
-    const char* tab = reinterpret_cast<const char*>(P.tables + (int64_t)b * P.T_lib + P.offE[E]);
-    const int t0 = (E - 1) * P.tau;
-    const int n = P.Lk - t0 - P.hrz;
-    const int nch = (n + ROWS - 1) / ROWS;
-    auto issue = [&](int ci, uint32_t slot) {
-        const int rows = min(ROWS, n - ci * ROWS);
-        tma_load_1d(R.buf + slot * (LK_CHUNK / 16), tab + (int64_t)ci * CB, (uint32_t)(rows * kp * 8), R.bar + slot);
-    };
-    if (lane == 0) {
-        fence_proxy_async();
-#pragma unroll
-        for (int i = 0; i < LK_STAGES; ++i)
-            if (i < nch) issue(i, (R.it + i) % LK_STAGES);
-    }
-    double Sp0 = 0.0, Spp0 = 0.0, Spo0 = 0.0, Sp1 = 0.0, Spp1 = 0.0, Spo1 = 0.0;
-    const __half2* Yo = Y + (int64_t)(t0 + P.oshift) * 32 + lane;
-    const char* Yb = reinterpret_cast<const char*>(Y);
-    uint32_t lbase = (uint32_t)((P.gshift * 32 + lane) * sizeof(__half2));
-    asm("" : "+r"(lbase));
-    auto Yl = [&](uint32_t idx) { return __half22float2(*reinterpret_cast<const __half2*>(Yb + (idx * 128u + lbase))); };
-    float2 c = make_float2(0.f, 0.f);
-    for (int ci = 0; ci < nch; ++ci) {
-        const uint32_t slot = R.it % LK_STAGES;
-        mbar_wait(R.bar + slot, (R.it / LK_STAGES) & 1u);
-        const uint4* rowp = R.buf + slot * (LK_CHUNK / 16);
-        const int r0 = ci * ROWS, r1 = min(n, r0 + ROWS);
-        float2 sp = make_float2(0.f, 0.f), spp = sp, spo = sp;
-#pragma unroll LK_UNROLL
-        for (int r = r0; r < r1; ++r) {
-            const uint4* row = rowp + (r - r0) * (kp / 2);
-            float2 p = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int j2 = 0; j2 < kp / 2; ++j2) {
-                const uint4 e2 = row[j2];
-                CCM_CHECK((int)e2.x + P.gshift >= 0 && (int)e2.x + P.gshift < P.Lt);
-                p = f2fma(__uint_as_float(e2.y), Yl(e2.x), p);
-                if (2 * j2 + 1 < k) p = f2fma(__uint_as_float(e2.w), Yl(e2.z), p);
-            }
-            if (r == 0) c = p;
-            p.x -= c.x;
-            p.y -= c.y;
-            const float2 o = __half22float2(Yo[(int64_t)r * 32]);
-            sp.x += p.x;
-            sp.y += p.y;
-            spp.x = fmaf(p.x, p.x, spp.x);
-            spp.y = fmaf(p.y, p.y, spp.y);
-            spo.x = fmaf(p.x, o.x, spo.x);
-            spo.y = fmaf(p.y, o.y, spo.y);
-        }
-        Sp0 += (double)sp.x; Spp0 += (double)spp.x; Spo0 += (double)spo.x;
-        Sp1 += (double)sp.y; Spp1 += (double)spp.y; Spo1 += (double)spo.y;
-        __syncwarp();
-        ++R.it;
-        if (lane == 0 && ci + LK_STAGES < nch) {
-            fence_proxy_async();
-            issue(ci + LK_STAGES, slot);
-        }
-    }
-    const double nn = (double)n;
-    auto finish = [&](int col, int pcol, double Sp, double Spp, double Spo) {
-        if (col < 0) return;
-        const double2 st = P.stats[(int64_t)(E - 1) * P.Np + pcol];
-        const bool o_const = P.cflag[(int64_t)(E - 1) * P.Np + pcol] != 0;
-        const double cov = Spo - Sp * st.x / nn;
-        const double vp = Spp - Sp * Sp / nn;
-        const double vo = st.y - st.x * st.x / nn;
-        float r = CUDART_NAN_F;
-        if (!o_const && vp > 0.0 && vo > 0.0) r = (float)(cov / sqrt(vp * vo));
-        P.rho[((int64_t)P.slotRow[b] - P.rbase) * P.rstride + P.roff + col] = r;
-    };
-    finish(col0, tile * TILE_H + 2 * lane, Sp0, Spp0, Spo0);
-    finish(col1, tile * TILE_H + 2 * lane + 1, Sp1, Spp1, Spo1);
-}
-
-__device__ __forceinline__ void lookup_dispatch_h(int E, const LookupParams& P, const __half2* Y, int tile, int b,
-                                                  int lane, int col0, int col1, WarpRing& R) {
-    switch (E) {
-#define CCM_CASE(e) case e: lookup_one_h<e>(P, Y, tile, b, lane, col0, col1, R); break;
-        CCM_CASE(1) CCM_CASE(2) CCM_CASE(3) CCM_CASE(4) CCM_CASE(5) CCM_CASE(6) CCM_CASE(7)
-        CCM_CASE(8) CCM_CASE(9) CCM_CASE(10) CCM_CASE(11) CCM_CASE(12) CCM_CASE(13) CCM_CASE(14)
-        CCM_CASE(15) CCM_CASE(16) CCM_CASE(17) CCM_CASE(18) CCM_CASE(19) CCM_CASE(20)
-#undef CCM_CASE
-        default: break;
-    }
-}
-
 constexpr size_t lookup_ring_bytes() { return (size_t)LOOKUP_WARPS * LK_STAGES * (LK_CHUNK + 8) + 16; }
 
 // grid = ntiles; block = LOOKUP_WARPS * 32. SMEM = true: the 32-column target tile
@@ -1126,8 +994,7 @@ constexpr size_t lookup_ring_bytes() { return (size_t)LOOKUP_WARPS * LK_STAGES *
 // reuse); SMEM = false (long series): gathers straight from L2/HBM. Tiles run in reverse
 // order so that the expensive high-E tiles (target mode) start first.
 // Dynamic smem: [tile: L*32 floats if SMEM][ring: LOOKUP_WARPS*2*LK_CHUNK][bars].
-// HALF (EDM_LOOKUP_FP16, requires SMEM): 64-target fp16 tiles (yh_index), lanes = target pairs.
-template <bool SMEM, bool HALF = false>
+template <bool SMEM>
 __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupParams P) {
     extern __shared__ __align__(16) unsigned char lk_smem[];
     // CTAs 0 .. ntiles-nsplit-1 take whole tiles from the last (target mode: highest E, the
@@ -1161,8 +1028,7 @@ __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupPara
     }
     const float* Y;
     int64_t ys;
-    // the tile's contiguous [L][32] block of 4-byte words (fp32 targets, or half2 target pairs)
-    const float* src = P.Yp + (int64_t)tile * P.Lt * 32;
+    const float* src = P.Yp + yp_index(tile * TILE_J, 0, P.Lt);  // the tile's contiguous [L][32] block
     if (SMEM) {
         // the tile's contiguous [L][32] block staged by TMA bulk copies (cp.async.bulk, 32 KB each)
         // completing on one mbarrier; every thread waits on its phase 0
@@ -1185,20 +1051,6 @@ __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupPara
     }
     ys = TILE_J;
     __syncthreads();
-    if (HALF) {
-        const int col0 = P.colmap[tile * TILE_H + 2 * lane], col1 = P.colmap[tile * TILE_H + 2 * lane + 1];
-        for (int b = part * LOOKUP_WARPS + warp; b < P.B; b += parts * LOOKUP_WARPS) {
-            const int E = P.tileE ? Et : P.slotE[b];
-            if (E > P.Eok) {
-                const int64_t o = ((int64_t)P.slotRow[b] - P.rbase) * P.rstride + P.roff;
-                if (col0 >= 0) P.rho[o + col0] = CUDART_NAN_F;
-                if (col1 >= 0) P.rho[o + col1] = CUDART_NAN_F;
-                continue;
-            }
-            lookup_dispatch_h(E, P, reinterpret_cast<const __half2*>(Y), tile, b, lane, col0, col1, R);
-        }
-        return;
-    }
     const int col = P.colmap[tile * TILE_J + lane];
     for (int b = part * LOOKUP_WARPS + warp; b < P.B; b += parts * LOOKUP_WARPS) {
         const int E = P.tileE ? Et : P.slotE[b];

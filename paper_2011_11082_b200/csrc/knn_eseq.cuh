@@ -42,9 +42,6 @@ __device__ unsigned long long esq_stats[ECAP + 1][8];
 #ifndef CCM_ESQ_RANKSORT
 #define CCM_ESQ_RANKSORT 1   // rank-count sort of the first batch (else the bitonic network): -1.5 % / -5 %
 #endif
-#ifndef CCM_ESQ_MINCTAS
-#define CCM_ESQ_MINCTAS 5    // resident CTAs per SM the register budget must allow (96 registers)
-#endif
 #ifndef CCM_ESQ_PAIRF32
 #define CCM_ESQ_PAIRF32 0    // paired 8-byte loads in the fp32 recompute (tau = 1)
 #endif
@@ -571,7 +568,7 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
 // Requires: every E in 1..Etop selected (P.maskS), no library-mode slotE, no candidate mask, the
 // series in shared memory, ncand <= 32 NC.
 template <int MODE, bool TAU1, int NC>
-__global__ void __launch_bounds__(ESQ_WARPS * 32, CCM_ESQ_MINCTAS) knn_eseq_kernel(KnnParams P) {
+__global__ void __launch_bounds__(ESQ_WARPS * 32, KNN_MIN_CTAS) knn_eseq_kernel(KnnParams P) {
     extern __shared__ __align__(16) unsigned char esq_smem[];
     const int b = blockIdx.y;
     const int row = P.slot_series ? P.slot_series[b] : b;

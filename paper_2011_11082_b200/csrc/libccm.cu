@@ -115,8 +115,7 @@ inline int ccm_block(int64_t T_lib) {
 }
 constexpr int LOOKUP_SMEM_MAX = 227 * 1024;
 
-// target columns after per-E padding (to 32, or to 64 for the fp16 lookup's tiles)
-inline int64_t np_max(int N) { return (int64_t)(N + TILE_H - 1) / TILE_H * TILE_H + (int64_t)TILE_H * ECAP; }
+inline int64_t np_max(int N) { return (int64_t)(N + TILE_J - 1) / TILE_J * TILE_J + (int64_t)TILE_J * ECAP; }
 
 struct SimplexWs {
     int SB;         // series per phase-1 block: SIMPLEX_SLOTS, fewer when the lists exceed the budget
@@ -170,7 +169,6 @@ struct CcmWs {
     double* mean;       // [N]
     int* sexp;          // [N] sweep exponents (scan_kernel)
     int* texp;          // [N] target exponents (scan_kernel)
-    int* hexp;          // [N] fp16-lookup target exponents (scan_kernel)
     int* bad;           // [4] input-check counters (scan_kernel)
     int* libidx;        // [N] series of library row r (edm_ccm_rows' list)
     int* rsexp;         // [N] sweep exponent of library row r (list order)
@@ -202,7 +200,6 @@ CcmWs ccm_ws(void* base, int N, int L, int Lk, int tau, int hrz, int nlag) {
     w.mean = (double*)take((size_t)N * sizeof(double));
     w.sexp = (int*)take((size_t)N * sizeof(int));
     w.texp = (int*)take((size_t)N * sizeof(int));
-    w.hexp = (int*)take((size_t)N * sizeof(int));
     w.bad = (int*)take(4 * sizeof(int));
     w.libidx = (int*)take((size_t)N * sizeof(int));
     w.rsexp = (int*)take((size_t)N * sizeof(int));
@@ -389,11 +386,11 @@ edm_status pad_series(const float* X, int64_t ldx, const int* slot_series, const
 // S0 input check (scan_kernel) of series [c0, c0 + n): enqueue the scan and the copy of its
 // counters to `hbad` (host int[4]); the caller synchronises and calls check_bad.
 edm_status launch_scan(const edm_dataset& ds, int c0, int n, int* sexp, double* mean, int* texp, int* dbad, int* hbad,
-                       cudaStream_t cs, int* hexp = nullptr) {
+                       cudaStream_t cs) {
     static const int init[4] = {0, 0, 0x7fffffff, 0};
     CUDA_TRY(cudaMemcpyAsync(dbad, init, sizeof(init), cudaMemcpyHostToDevice, cs));
     if (n > 0) {
-        PROF_LAUNCH(EDM_PROF_PREP, cs, scan_kernel<<<(n + 127) / 128, 128, 0, cs>>>(ds.data, ds.ld, c0, n, ds.L, sexp, mean, texp, dbad, hexp));
+        PROF_LAUNCH(EDM_PROF_PREP, cs, scan_kernel<<<(n + 127) / 128, 128, 0, cs>>>(ds.data, ds.ld, c0, n, ds.L, sexp, mean, texp, dbad));
         LAUNCH_CHECK("scan_kernel");
     }
     CUDA_TRY(cudaMemcpyAsync(hbad, dbad, 4 * sizeof(int), cudaMemcpyDeviceToHost, cs));
@@ -698,7 +695,7 @@ inline size_t tdist_bytes(const CcmWs& w) { return align_up((size_t)w.B * w.T_li
 edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int m_hi, int lag_min, int lag_max,
                     edm_e_mode mode, int32_t exclude_self, int32_t lib_begin, int32_t lib_end, float* rho,
                     void* workspace, size_t ws_bytes, size_t need, cudaStream_t cs, const ConvArgs* cv = nullptr,
-                    const TablesOut* to = nullptr, const int32_t* lib_list = nullptr, bool fp16 = false) {
+                    const TablesOut* to = nullptr, const int32_t* lib_list = nullptr) {
     if (need == 0 || ws_bytes < need) return fail(EDM_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
     edm_status st = check_device();
     if (st != EDM_OK) return st;
@@ -711,7 +708,7 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
     // ---- S0 input check of the whole dataset (every series is a target) with the per-series
     // sweep / target exponents and means; E[] is validated on the host: one synchronisation
     int hbad[4];
-    st = launch_scan(ds, 0, N, W.sexp, W.mean, W.texp, W.bad, hbad, cs, fp16 ? W.hexp : nullptr);
+    st = launch_scan(ds, 0, N, W.sexp, W.mean, W.texp, W.bad, hbad, cs);
     if (st != EDM_OK) return st;
     std::vector<int32_t> hE(N);
     CUDA_TRY(cudaMemcpyAsync(hE.data(), E, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, cs));
@@ -736,9 +733,7 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
     table_layout(Lk, tau, m_hi, offE, &T_lib);
 
     // target ordering (S5): target mode -> stable counting sort by (E_j, j), every E segment
-    // padded to a multiple of the tile width (32 targets, 64 for the fp16 lookup) so that a tile has
-    // one E; library mode -> identity.
-    const int TILE = fp16 ? TILE_H : TILE_J;
+    // padded to a multiple of 32 so that a 32-target tile has one E; library mode -> identity.
     std::vector<int> colmap, tileE;
     if (mode == EDM_E_TARGET) {
         std::vector<int> cnt(ECAP + 2, 0);
@@ -747,21 +742,21 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
         int64_t pos = 0;
         for (int e = 1; e <= ECAP; ++e) {
             seg[e] = (int)pos;
-            const int nt = (cnt[e] + TILE - 1) / TILE;
+            const int nt = (cnt[e] + TILE_J - 1) / TILE_J;
             for (int t = 0; t < nt; ++t) tileE.push_back(e);
-            pos += (int64_t)nt * TILE;
+            pos += (int64_t)nt * TILE_J;
         }
         colmap.assign(pos, -1);
         std::vector<int> fill(seg);
         for (int j = 0; j < N; ++j) colmap[fill[hE[j]]++] = j;
     } else {
-        const int nt = (N + TILE - 1) / TILE;
-        colmap.assign((size_t)nt * TILE, -1);
+        const int nt = (N + TILE_J - 1) / TILE_J;
+        colmap.assign((size_t)nt * TILE_J, -1);
         for (int j = 0; j < N; ++j) colmap[j] = j;
         tileE.assign(nt, 0);
     }
     const int ntiles = (int)tileE.size();
-    const int Np = ntiles * TILE;
+    const int Np = ntiles * TILE_J;
     // library slots: row r of this call is series lib(r) = lib_list[r] (edm_ccm_rows) or lib_begin + r
     const int nlib = lib_end - lib_begin;
     auto lib = [&](int r) { return lib_list ? lib_list[r] : lib_begin + r; };
@@ -808,16 +803,13 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
         LAUNCH_CHECK("transpose_kernel");
         if (!to) {
             dim3 pg((Np + 255) / 256, std::min(L, 256));
-            if (fp16) PROF_LAUNCH(EDM_PROF_PREP, cs, permute_half_kernel<<<pg, 256, 0, cs>>>(ds.data, ds.ld, L, Np, W.colmap, W.mean, W.hexp,
-                                                                                           reinterpret_cast<__half*>(W.Yp)));
-            else PROF_LAUNCH(EDM_PROF_PREP, cs, permute_kernel<<<pg, 256, 0, cs>>>(ds.data, ds.ld, L, Np, W.colmap, W.mean, W.texp, W.Yp));
+            PROF_LAUNCH(EDM_PROF_PREP, cs, permute_kernel<<<pg, 256, 0, cs>>>(ds.data, ds.ld, L, Np, W.colmap, W.mean, W.texp, W.Yp));
             LAUNCH_CHECK("permute_kernel");
             for (int l = lag_min; l <= lag_max; ++l) {
                 const int64_t so = (int64_t)(l - lag_min) * ECAP * W.Npm;
                 PROF_LAUNCH(EDM_PROF_PREP, cs,
                             stats_kernel<<<(Np + 127) / 128, 128, 0, cs>>>(W.Yp, L, ds.data, ds.ld, W.colmap, Np, tau, m_lo + l,
-                                                                          L - 1 - m_hi + l, ECAP, W.stats + so, W.cflag + so,
-                                                                          fp16 ? reinterpret_cast<const __half*>(W.Yp) : nullptr));
+                                                                          L - 1 - m_hi + l, ECAP, W.stats + so, W.cflag + so));
                 LAUNCH_CHECK("stats_kernel");
             }
         }
@@ -827,10 +819,7 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
     const size_t tile_smem = (size_t)L * TILE_J * sizeof(float);
     const bool use_smem = tile_smem + lookup_ring_bytes() <= (size_t)LOOKUP_SMEM_MAX;
     const size_t lk_smem = (use_smem ? tile_smem : 0) + lookup_ring_bytes();
-    if (fp16 && !use_smem)
-        return fail(EDM_EUNSUPPORTED, "the fp16 lookup stages the target tile in shared memory: L=%d is too long", L);
-    if (fp16) CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
-    else if (use_smem) CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
+    if (use_smem) CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
     else CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
     const bool gser = knn_use_gser(Lk, tau);
     if (cv) return conv_blocks(ds, W, offE, T_lib, maskS, tau, m_hi, mode, exclude_self, row_sexp, nlib, ntiles, Np,
@@ -871,8 +860,7 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
             Q.rho = rho; Q.rstride = (int64_t)nlag * N; Q.roff = (int64_t)(l - lag_min) * N;
             Q.rbase = 0; Q.Eok = ECAP;
             lookup_split(ntiles, nb, sc, Q);
-            if (fp16) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true, true><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
-            else if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+            if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
             else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
             LAUNCH_CHECK("lookup_kernel");
         }
@@ -894,19 +882,6 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int3
     const size_t need = edm_workspace_bytes(1, ds.N, ds.L, ECAP, tau, Tp);
     return ccm_core(ds, E, tau, 0, Tp, Tp, Tp, mode, exclude_self, lib_begin, lib_end, rho, workspace, ws_bytes, need,
                     (cudaStream_t)stream);
-}
-
-edm_status edm_ccm_all_pairs_ex(edm_dataset ds, const int32_t* E, int32_t tau, int32_t Tp, edm_e_mode mode,
-                                int32_t exclude_self, int32_t lib_begin, int32_t lib_end, uint32_t flags, float* rho,
-                                void* workspace, size_t ws_bytes, void* stream) {
-    if (flags & ~(uint32_t)EDM_LOOKUP_FP16) return fail(EDM_EINVAL, "unknown flags 0x%x", flags);
-    if (!ds.data || !E || !rho || !workspace) return fail(EDM_EINVAL, "null pointer");
-    if (ds.N < 1 || ds.L < 2 || ds.ld < ds.N || tau < 1 || Tp < 0 || (mode != EDM_E_TARGET && mode != EDM_E_LIBRARY))
-        return fail(EDM_EINVAL, "bad arguments N=%d L=%d ld=%lld tau=%d Tp=%d mode=%d", ds.N, ds.L, (long long)ds.ld, tau, Tp, (int)mode);
-    if (lib_begin < 0 || lib_end > ds.N || lib_begin > lib_end) return fail(EDM_EINVAL, "bad library range [%d,%d)", lib_begin, lib_end);
-    const size_t need = edm_workspace_bytes(1, ds.N, ds.L, ECAP, tau, Tp);
-    return ccm_core(ds, E, tau, 0, Tp, Tp, Tp, mode, exclude_self, lib_begin, lib_end, rho, workspace, ws_bytes, need,
-                    (cudaStream_t)stream, nullptr, nullptr, nullptr, (flags & EDM_LOOKUP_FP16) != 0);
 }
 
 edm_status edm_ccm_rows(edm_dataset ds, const int32_t* E, int32_t tau, int32_t Tp, edm_e_mode mode,

@@ -28,13 +28,12 @@ from . import build as _build
 
 EDM_OK, EDM_EINVAL, EDM_ETOOSHORT, EDM_EWORKSPACE, EDM_ECUDA, EDM_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 EDM_E_TARGET, EDM_E_LIBRARY = 0, 1
-EDM_LOOKUP_FP16 = 1
 E_CAP = 20
 
 EXPORTS = ("edm_embed_knn", "edm_simplex_optimal_E", "edm_ccm_all_pairs", "edm_workspace_bytes",
            "edm_causal_map_host", "edm_last_error", "edm_version", "edm_profile_begin", "edm_profile_end",
            "edm_ccm_lagged", "edm_ccm_lagged_workspace_bytes", "edm_ccm_convergence",
-           "edm_ccm_convergence_workspace_bytes", "edm_ccm_tables", "edm_ccm_tables_workspace_bytes", "edm_ccm_rows", "edm_ccm_all_pairs_ex")
+           "edm_ccm_convergence_workspace_bytes", "edm_ccm_tables", "edm_ccm_tables_workspace_bytes", "edm_ccm_rows")
 PROF_KINDS = ("prep", "simplex_knn", "simplex_rho", "ccm_knn", "lookup", "other")
 
 
@@ -84,8 +83,6 @@ def load(path: Optional[str] = None):
                                         sz, vp]
     lib.edm_ccm_convergence_workspace_bytes.restype = sz
     lib.edm_ccm_convergence_workspace_bytes.argtypes = [i32, i32, i32, i32, i32, i32]
-    lib.edm_ccm_all_pairs_ex.restype = i32
-    lib.edm_ccm_all_pairs_ex.argtypes = [edm_dataset, vp, i32, i32, i32, i32, i32, i32, C.c_uint32, vp, vp, sz, vp]
     lib.edm_ccm_rows.restype = i32
     lib.edm_ccm_rows.argtypes = [edm_dataset, vp, i32, i32, i32, i32, vp, i32, vp, vp, sz, vp]
     lib.edm_ccm_tables.restype = i32
@@ -193,10 +190,8 @@ def _mode(mode) -> int:
 
 def ccm_all_pairs(data: torch.Tensor, E: torch.Tensor, tau: int = 1, Tp: int = 1, mode="target",
                   exclude_self: bool = True, lib_begin: int = 0, lib_end: Optional[int] = None,
-                  out: Optional[torch.Tensor] = None, lookup: str = "fp32") -> torch.Tensor:
-    """Phase 2: rho[i - lib_begin, j] for library rows [lib_begin, lib_end) and all targets j.
-    lookup="fp16": edm_ccm_all_pairs_ex with EDM_LOOKUP_FP16 (reduced-precision targets, not the
-    headline; see include/libccm.h)."""
+                  out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Phase 2: rho[i - lib_begin, j] for library rows [lib_begin, lib_end) and all targets j."""
     ds = _dataset(data)
     _require_cuda(E, torch.int32, "E")
     E = E.contiguous()
@@ -211,15 +206,8 @@ def ccm_all_pairs(data: torch.Tensor, E: torch.Tensor, tau: int = 1, Tp: int = 1
         if not out.is_contiguous() or out.numel() < rows * ds.N:
             raise ValueError("out must be contiguous with at least rows*N elements")
     ws = workspace(1, ds.N, ds.L, E_CAP, tau, Tp, data.device)
-    if lookup == "fp32":
-        _check(load().edm_ccm_all_pairs(ds, E.data_ptr(), tau, Tp, _mode(mode), int(exclude_self), lib_begin, lib_end,
-                                        out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(data.device)))
-    elif lookup == "fp16":
-        _check(load().edm_ccm_all_pairs_ex(ds, E.data_ptr(), tau, Tp, _mode(mode), int(exclude_self), lib_begin,
-                                           lib_end, EDM_LOOKUP_FP16, out.data_ptr(), ws.data_ptr(), ws.numel(),
-                                           _stream(data.device)))
-    else:
-        raise ValueError(f"lookup must be 'fp32' or 'fp16', got {lookup!r}")
+    _check(load().edm_ccm_all_pairs(ds, E.data_ptr(), tau, Tp, _mode(mode), int(exclude_self), lib_begin, lib_end,
+                                    out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(data.device)))
     return out
 
 

@@ -316,32 +316,3 @@ def test_ccm_rows_list_equals_range_rows():
     order = np.concatenate(parts)
     full = libccm.ccm_all_pairs(d, E, 1, 1, "library").cpu().numpy()
     assert np.array_equal(got.view(np.uint32), full[order].view(np.uint32))
-
-
-# ---------------------------------------------------------------- EDM_LOOKUP_FP16 (optional, not the headline)
-def check_ccm_fp16(data, E, tau=1, Tp=1, mode="target", lib_begin=0, lib_end=None, tol=RHO_TOL):
-    N = data.shape[1]
-    lib_end = N if lib_end is None else lib_end
-    g = libccm.ccm_all_pairs(dev(data), dev(E, torch.int32), tau, Tp, mode, True, lib_begin, lib_end, lookup="fp16")
-    ref = O.ccm_rows(data, E, tau, Tp, 0 if mode == "target" else 1, True, lib_begin, lib_end)
-    return assert_rho_close(g.cpu().numpy(), ref, tol)
-
-
-def test_fp16_lookup_within_bar():
-    """The fp16-target lookup (64-target tiles, half2 gathers) stays within the 1e-4 rho bar:
-    ragged N (64-wide E segments), both modes, Tp 0/1, a constant series (NaN), c3-shaped rows."""
-    data = synth.random_dataset(45, 150, 11)
-    data[:, 9] = 0.75
-    E = np.random.default_rng(3).integers(1, 8, 45).astype(np.int32)
-    errs = []
-    for mode in ("target", "library"):
-        for Tp in (0, 1):
-            errs.append(check_ccm_fp16(data, E, 1, Tp, mode))
-    c3 = synth.make_config("c3", N=4096)
-    E3 = libccm.simplex_optimal_E(dev(c3), 20).cpu().numpy()
-    errs.append(check_ccm_fp16(c3, E3, 1, 1, "target", 1000, 1004))
-    assert max(errs) > 0.0  # it is a different (reduced-precision) computation
-    with pytest.raises(libccm.EdmError) as e:  # the fp16 tiles live in shared memory only
-        libccm.ccm_all_pairs(dev(synth.make_config("c5", N=8, L=2100)), dev(np.full(8, 2), torch.int32),
-                             lookup="fp16")
-    assert e.value.status == libccm.EDM_EUNSUPPORTED
