@@ -628,7 +628,7 @@ def main():
             "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": vs_base, "vs_baseline_ref": PAPER_C3_REF if vs_base else None,
-            "dtype": "f64 kNN / f32 lookup", "data": "synthetic",
+            "dtype": "f32 kNN certified against f64 keys / f32 lookup", "data": "synthetic",
             "config": {"workload": f"{args.config}: {N} series x L={L}, E=1..{E_max}, tau={tau}, Tp={Tp}, "
                                    f"mode={args.mode}, exclude_self", "N": N, "L": L,
                        "parallelism": f"library rows / series sharded over {world} GPU(s)",
