@@ -210,3 +210,29 @@ def test_unrescalable_series_unsupported():
     with pytest.raises(libccm.EdmError) as e:
         libccm.simplex_optimal_E(dev(data), 4)
     assert e.value.status == libccm.EDM_EUNSUPPORTED
+
+
+def test_eseq_and_sweep_kernels_build_identical_tables():
+    """The E-sequential kNN (default when every E in 1..Etop is selected) and the round-1 sweep
+    kernel (CCM_KNN_ALGO=sweep) are two schedules of the same selection: identical labels and
+    distances, weights within 1e-6, on c2 with every E = 1..20 and on quantised data (ties)."""
+    for data in (synth.make_config("c2", N=300), synth.quantise8(synth.make_config("c2", N=120, L=500))):
+        N = data.shape[1]
+        d = dev(data)
+        E = dev((1 + np.arange(N) % 20).astype(np.int32), torch.int32)
+        for Eq in (1, 2, 3, 9, 20):
+            a = libccm.ccm_tables(d, E, Eq)
+            os.environ["CCM_KNN_ALGO"] = "sweep"
+            try:
+                b = libccm.ccm_tables(d, E, Eq)
+            finally:
+                del os.environ["CCM_KNN_ALGO"]
+            assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]), Eq
+            assert float((a[2] - b[2]).abs().max()) <= 1e-6
+        sa = libccm.simplex_optimal_E(d, 20, return_rho=True)
+        os.environ["CCM_KNN_ALGO"] = "sweep"
+        try:
+            sb = libccm.simplex_optimal_E(d, 20, return_rho=True)
+        finally:
+            del os.environ["CCM_KNN_ALGO"]
+        assert torch.equal(sa[0], sb[0]) and torch.equal(sa[1].view(torch.int32), sb[1].view(torch.int32))
