@@ -243,6 +243,10 @@ struct KnnParams {
     // MODE_CCM table readback (edm_ccm_tables): fp32(sqrt(d2)) of every table entry, same
     // layout as `tables` (NULL in the hot path)
     float* tdist;
+    // long series (knn_long_kernel): sorted order of slot b's candidate values
+    const unsigned short* lng_slab;   // [slot][lng_lds]: labels in value order
+    const unsigned short* lng_pos;    // [slot][lng_lds]: rank of each label
+    int64_t lng_lds;
 };
 
 // knn_kernel series variants: shared-memory copy, shared-memory copy + library-set mask
@@ -321,7 +325,10 @@ constexpr size_t knn_smem_bytes(int L, int tau) {
     return (size_t)KNN_WARPS * knn_warp_bytes(L) + (size_t)(knn_padl(tau) + L + KNN_PADR) * sizeof(float);
 }
 constexpr size_t knn_smem_bytes_gser(int L) { return (size_t)KNN_WARPS * knn_warp_bytes(L); }
-__host__ __device__ constexpr int64_t knn_ldpad(int L, int tau) { return ((int64_t)knn_padl(tau) + L + KNN_PADR + 3) / 4 * 4; }
+// padded global copies cover whole 1,536-candidate super-chunks (knn_long_kernel reads them)
+__host__ __device__ constexpr int64_t knn_ldpad(int L, int tau) {
+    return ((int64_t)knn_padl(tau) + (L + 1535) / 1536 * 1536 + KNN_PADR + 3) / 4 * 4;
+}
 
 // Padded global copies for KNN_GSER: out[b * ldpad + padl + t] = X[row_b * ldx + t] for
 // t in [0, L), 1e30 elsewhere (row_b = slot_series[b] or b), rescaled by 2^sexp[row_b].

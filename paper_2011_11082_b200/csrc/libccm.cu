@@ -14,6 +14,7 @@
 
 #include "ccm_kernels.cuh"
 #include "knn_eseq.cuh"
+#include "knn_long.cuh"
 #include "libccm.h"
 
 using namespace ccm;
@@ -125,6 +126,9 @@ struct SimplexWs {
     double* pred;   // [SB][ECAP][LQ]
     double* rho;    // [SB][E_max]
     float* Xpad;    // [SB][knn_ldpad(L, tau)] padded copies (long series)
+    unsigned short* lslab;  // [SB][llds] sorted candidate order (long series)
+    unsigned short* lpos;   // [SB][llds]
+    int64_t llds;
     double* sd2;    // [SB][S_slot] sorted lists (squared distances)
     int* ss;        // [SB][S_slot] sorted lists (library indices)
     int64_t S_slot;
@@ -143,8 +147,10 @@ SimplexWs simplex_ws(void* base, int N, int L, int E_max, int tau) {
         if (E <= ECAP) acc += (int64_t)(E + 1) * LQ;
     }
     w.S_slot = acc;
+    const int64_t llds = (L + 7) / 8 * 8;
     const size_t per_slot = (size_t)L * sizeof(float) + (size_t)ECAP * LQ * sizeof(double) +
-                            (size_t)acc * (sizeof(double) + sizeof(int)) + (size_t)knn_ldpad(L, tau) * sizeof(float);
+                            (size_t)acc * (sizeof(double) + sizeof(int)) + (size_t)knn_ldpad(L, tau) * sizeof(float) +
+                            (size_t)llds * 4;
     const int SB = (int)std::max<size_t>(1, std::min<size_t>({(size_t)N, (size_t)SIMPLEX_SLOTS, SIMPLEX_LIST_BUDGET / per_slot}));
     w.SB = SB;
     size_t off = 0;
@@ -155,6 +161,9 @@ SimplexWs simplex_ws(void* base, int N, int L, int E_max, int tau) {
     w.pred = (double*)(b + off); off += align_up((size_t)SB * ECAP * LQ * sizeof(double));
     w.rho = (double*)(b + off);  off += align_up((size_t)SB * std::max(E_max, 1) * sizeof(double));
     w.Xpad = (float*)(b + off);  off += align_up((size_t)SB * knn_ldpad(L, tau) * sizeof(float));
+    w.llds = llds;
+    w.lslab = (unsigned short*)(b + off); off += align_up((size_t)SB * llds * 2);
+    w.lpos = (unsigned short*)(b + off);  off += align_up((size_t)SB * llds * 2);
     w.sd2 = (double*)(b + off);  off += align_up((size_t)SB * acc * sizeof(double));
     w.ss = (int*)(b + off);      off += align_up((size_t)SB * acc * sizeof(int));
     w.bytes = off;
@@ -179,6 +188,9 @@ struct CcmWs {
     int* slotE;         // [N]
     uint2* tables;      // [B][T_lib]
     float* Xpad;        // [B][knn_ldpad(Lk, tau)] padded library series (long series)
+    unsigned short* lslab;  // [B][llds] sorted candidate order (knn_long_kernel)
+    unsigned short* lpos;   // [B][llds]
+    int64_t llds;
     int64_t Npm, T_lib;
     int B;              // libraries per block (ccm_block)
     size_t bytes;
@@ -211,6 +223,9 @@ CcmWs ccm_ws(void* base, int N, int L, int Lk, int tau, int hrz, int nlag) {
     w.B = ccm_block(w.T_lib);
     w.tables = (uint2*)take((size_t)w.B * w.T_lib * sizeof(uint2));
     w.Xpad = (float*)take((size_t)w.B * knn_ldpad(Lk, tau) * sizeof(float));
+    w.llds = (Lk + 7) / 8 * 8;
+    w.lslab = (unsigned short*)take((size_t)w.B * w.llds * 2);
+    w.lpos = (unsigned short*)take((size_t)w.B * w.llds * 2);
     w.bytes = off;
     return w;
 }
@@ -297,8 +312,33 @@ template <int MODE>
 bool esq_eligible(const KnnParams& P, bool full, int ncand) {
     const char* env = getenv("CCM_KNN_ALGO");
     if (env && !strcmp(env, "sweep")) return false;
-    return full && !P.slotE && !P.allow && !P.Xpad && ncand >= 1 && ncand <= 32 * ESQ_NCMAX &&
+    return full && !P.slotE && !P.allow && ncand >= 1 && ncand <= 32 * ESQ_NCMAX &&
            esq_smem_bytes(P.tau, ESQ_NCMAX, P.L) <= (size_t)227 * 1024;
+}
+// knn_long_kernel: the same conditions for longer series, with the padded global copy and the
+// sorted candidate order prepared (P.Xpad, P.lng_slab)
+bool long_eligible(const KnnParams& P, bool full, int ncand) {
+    const char* env = getenv("CCM_KNN_ALGO");
+    if (env && !strcmp(env, "sweep")) return false;
+    return full && !P.slotE && !P.allow && P.Xpad && P.lng_slab && ncand > 32 * ESQ_NCMAX && ncand <= LNG_SORT_MAX;
+}
+template <int MODE, bool TAU1>
+edm_status launch_long_t(const KnnParams& P, dim3 grid, cudaStream_t st) {
+    PROF_LAUNCH(MODE == MODE_CCM ? EDM_PROF_CCM_KNN : EDM_PROF_SIMPLEX_KNN, st,
+                knn_long_kernel<MODE, TAU1><<<grid, LNG_WARPS * 32, 0, st>>>(P));
+    LAUNCH_CHECK("knn_long_kernel");
+    return EDM_OK;
+}
+// the sorted candidate order of every slot of a block (knn_long_kernel's E = 1 seeds)
+edm_status sort_series(const float* Xpad, int64_t ldpad, int tau, int ncand, int nslots, unsigned short* slab,
+                       unsigned short* pos, int64_t lds, cudaStream_t cs) {
+    int P2 = 32;
+    while (P2 < ncand) P2 <<= 1;
+    const size_t smem = (size_t)P2 * 8;
+    CUDA_TRY(cudaFuncSetAttribute(sort_series_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PROF_LAUNCH(EDM_PROF_PREP, cs, sort_series_kernel<<<nslots, 512, smem, cs>>>(Xpad, ldpad, knn_padl(tau), ncand, P2, slab, pos, lds));
+    LAUNCH_CHECK("sort_series_kernel");
+    return EDM_OK;
 }
 
 // Picks the specialisation: tau == 1 (constant-offset shared loads), whether every E in
@@ -313,6 +353,12 @@ edm_status launch_knn(const KnnParams& P0, int nq, int slots, cudaStream_t st) {
     const bool full = !P.slotE && P.Etop >= 1 && P.maskS == ((2u << P.Etop) - 2u);
     if constexpr (MODE != MODE_EMBED) {
         const int ncand = MODE == MODE_SIMPLEX ? (P.L + 1) / 2 - 1 : P.L - P.Tp;
+        if (long_eligible(P, full, ncand)) {
+            const int nc = std::max(1, (nq + LNG_WARPS * KNN_QPW - 1) / (LNG_WARPS * KNN_QPW));
+            P.qpw = std::max(1, (nq + nc * LNG_WARPS - 1) / (nc * LNG_WARPS));
+            dim3 g((nq + LNG_WARPS * P.qpw - 1) / (LNG_WARPS * P.qpw), slots);
+            return P.tau == 1 ? launch_long_t<MODE, true>(P, g, st) : launch_long_t<MODE, false>(P, g, st);
+        }
         if (esq_eligible<MODE>(P, full, ncand)) {
             const char* qenv = getenv("CCM_ESQ_QPW");
             const int qmax = std::min(ESQ_QPW_MAX, qenv ? std::max(1, atoi(qenv)) : CCM_ESQ_QPW);
@@ -546,6 +592,12 @@ edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int
                 st = pad_series(W.Xs, L, nullptr, P.sexp, L, tau, nb, W.Xpad, cs);
                 if (st != EDM_OK) return st;
                 P.Xpad = W.Xpad; P.ldpad = knn_ldpad(L, tau);
+                const int ncand1 = (L + 1) / 2 - 1;
+                if (ncand1 > 32 * ESQ_NCMAX && ncand1 <= LNG_SORT_MAX) {
+                    st = sort_series(W.Xpad, P.ldpad, tau, ncand1, nb, W.lslab, W.lpos, W.llds, cs);
+                    if (st != EDM_OK) return st;
+                    P.lng_slab = W.lslab; P.lng_pos = W.lpos; P.lng_lds = W.llds;
+                }
             }
             st = launch_knn<MODE_SIMPLEX>(P, std::max(Ltgt - 1, 1), nb, cs);
             if (st != EDM_OK) return st;
@@ -838,6 +890,12 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
             st = pad_series(P.X, P.ldx, P.slot_series, P.sexp, Lk, tau, nb, W.Xpad, cs);
             if (st != EDM_OK) return st;
             P.Xpad = W.Xpad; P.ldpad = knn_ldpad(Lk, tau);
+            const int ncand2 = Lk - m_hi;
+            if (ncand2 > 32 * ESQ_NCMAX && ncand2 <= LNG_SORT_MAX && !P.slotE) {
+                st = sort_series(W.Xpad, P.ldpad, tau, ncand2, nb, W.lslab, W.lpos, W.llds, cs);
+                if (st != EDM_OK) return st;
+                P.lng_slab = W.lslab; P.lng_pos = W.lpos; P.lng_lds = W.llds;
+            }
         }
         st = launch_knn<MODE_CCM>(P, Lk - m_hi, nb, cs);
         if (st != EDM_OK) return st;

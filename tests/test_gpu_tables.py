@@ -236,3 +236,26 @@ def test_eseq_and_sweep_kernels_build_identical_tables():
         finally:
             del os.environ["CCM_KNN_ALGO"]
         assert torch.equal(sa[0], sb[0]) and torch.equal(sa[1].view(torch.int32), sb[1].view(torch.int32))
+
+
+def test_tables_long_series_kernel():
+    """Series longer than the register chunks (1,536 < candidates <= 16,384: knn_long_kernel,
+    super-chunks of 1,536 with exact per-E lists): tables bit-exact against the oracle, identical
+    to the sweep kernel's, and phase 1 equal to the oracle's; L = 3,000 (two super-chunks) and an
+    odd length with a ragged last super-chunk."""
+    for L, N in ((3000, 24), (4711, 12)):
+        data = synth.make_config("c5", N=N, L=L)
+        d = dev(data)
+        E = (1 + np.arange(N) % 20).astype(np.int32)
+        for Eq in (1, 2, 5, min(20, N)):
+            check_tables(data, E, Eq, np.arange(0, N, 5), d=d)
+            a = libccm.ccm_tables(d, dev(E, torch.int32), Eq)
+            os.environ["CCM_KNN_ALGO"] = "sweep"
+            try:
+                b = libccm.ccm_tables(d, dev(E, torch.int32), Eq)
+            finally:
+                del os.environ["CCM_KNN_ALGO"]
+            assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]), (L, Eq)
+        optE, rhoE = libccm.simplex_optimal_E(d, 20, 1, 0, 4, return_rho=True)
+        rE, rrho = O.simplex_all(data, 20, 1, 0, 4)
+        np.testing.assert_array_equal(optE.cpu().numpy(), rE)
