@@ -1,23 +1,27 @@
 // knn_eseq.cuh -- E-sequential kNN for the hot path (S1 phase-1 and S6-S8 phase-2 tables).
 //
-// Same result as knn_kernel (the k = E+1 smallest (d2, s) keys of C3/C4 at every E, every key
-// formed in fp64 in the oracle's operation order), different schedule:
-//   * one warp per run of consecutive queries t; lane l owns the candidates s = l + 32c and keeps
-//     their fp32 distances D_E(t, s) in REGISTERS, updated one E at a time (incremental over E,
-//     D_E = D_{E-1} + (x[t-(E-1)tau] - x[s-(E-1)tau])^2);
+// Same result as knn_kernel (the k = E+1 smallest (d2, s) keys of C3/C4 at every E, decided on
+// keys equal to the oracle's fp64 ones), different schedule:
+//   * one warp per run of consecutive queries t; lane l owns the candidate pairs s = 2l + 64c + {0,1}
+//     and keeps their fp32 distances D_E(t, s) in REGISTERS, updated one E at a time (incremental
+//     over E: D_E = D_{E-1} + (x[t-(E-1)tau] - x[s-(E-1)tau])^2, packed FFMA2);
 //   * before the update at E, a threshold T_E that provably admits every candidate of the exact
-//     top-k is formed from a few seed candidates: the successors s+1 of query t-1's list at E (the
-//     dynamics carries neighbourhoods along) and query t's own list at E-1 (neighbours at E-1 are
-//     mostly neighbours at E; their exact D_E is D_{E-1} plus one fp64 term); at E = 1, the
-//     neighbours of x[t] in a per-CTA sorted copy of the candidate values;
-//   * the sweep at E only flags the candidates with fp32 D_E <= T_E (typically k+1..k+3 of them),
-//     and those few are ranked exactly on fp64 keys recomputed in the oracle's order.
-// Threshold soundness: fp32 D~ of a sum of E <= 20 squared fp32 differences satisfies
+//     top-k is formed from a few seed candidates: the K = E+2 best carried from E-1 (one more fp32
+//     term each) and the successors s+1 of query t-1's list at E (the dynamics carries
+//     neighbourhoods along); at E = 1, the neighbours of x[t] in a per-CTA sorted copy of the
+//     candidate values;
+//   * the sweep at E only flags the candidates with fp32 D_E <= T_E (typically K + 5..8 of them);
+//     they are ranked on their fp32 values, and that order is CERTIFIED exact when adjacent values
+//     are separated by more than both fp32 error bands -- otherwise (near ties, exact ties of
+//     quantised data, tie floods) they are re-ranked on exact fp64 keys formed in the oracle's
+//     operation order.
+// Error bound: fp32 D~ of a sum of E <= 20 squared fp32 differences satisfies
 // |D~ - D| <= 2^-18 D + 2^-140 (relative (E+3) 2^-24 while normal; subnormal terms add at most
 // 2^-150 each; the sweep rescaling keeps everything below overflow), so a seed's exact D is at
 // most U = D~ (1 + 2^-17) + 2^-139; the k-th smallest U over >= k distinct valid seeds bounds the
 // k-th smallest exact D from above, and T = theta (1 + 2^-18) + 2^-140 (rounded up) admits every
-// candidate whose exact D is below it.
+// candidate whose exact D is below it; two fp32 values a < b whose gap exceeds
+// 2^-17 (a + b) + 2^-138 have exact keys in the same order.
 #pragma once
 #include "ccm_kernels.cuh"
 
