@@ -235,6 +235,35 @@ __device__ __forceinline__ bool fp32_separated(float a, float b) {
     return __fsub_rd(b, a) > __fadd_ru(__fmul_ru(__fadd_ru(a, b), 0x1p-17f), 0x1p-138f);
 }
 
+// Exact selection of the flagged candidates of one (query, E): the compacted labels W.buf[0..m)
+// when m <= ESQ_BUF, else the lanes' flag masks (pm0, pm1: bit b <-> esq_label(lane, b)); exact
+// fp64 keys in the oracle's order, merged into W.sD/W.sS (top K, ties -> lower label) with the
+// exact pre-test against the K-th key. Returns the list size. Kept out of line: it is the cold
+// path, and inlining it into every E-sequential instantiation costs instruction-cache misses.
+__device__ __noinline__ int esq_exact_select(EsqWarp& W, const float* __restrict__ qaf, const float* __restrict__ cbf,
+                                             int t, int E, int tau, int K, int m, unsigned pm0, unsigned pm1, int lane) {
+    int ecnt = 0;
+    for (int b0 = 0; (m > ESQ_BUF) ? __any_sync(FULL, (pm0 | pm1) != 0u) : b0 < m; b0 += 32) {
+        bool act;
+        int s = 0;
+        if (m > ESQ_BUF) {
+            act = (pm0 | pm1) != 0u;
+            if (act) {
+                int bb;
+                if (pm0) { bb = __ffs(pm0) - 1; pm0 &= pm0 - 1; }
+                else { bb = 32 + __ffs(pm1) - 1; pm1 &= pm1 - 1; }
+                s = esq_label(lane, bb);
+            }
+        } else {
+            act = b0 + lane < m;
+            if (act) s = W.buf[b0 + lane];
+        }
+        const double Dx = act ? esq_exact(qaf, cbf, t, s, E, tau) : CUDART_INF;
+        ecnt = esq_merge(W, ecnt, K, act, Dx, s, lane);
+    }
+    return ecnt;
+}
+
 // One warp, queries t_begin .. t_end-1 in order (see the file header). NC = register chunks.
 template <int MODE, bool TAU1, int NC>
 __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const float* __restrict__ qaf,
@@ -441,36 +470,9 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
                 }
                 if (m > ESQ_BUF || exact) {
                     // exact fp64 keys of every flagged candidate (near ties of the fp32 order, exact
-                    // ties of quantised data, tie floods): merged with the exact pre-test
+                    // ties of quantised data, tie floods): out of line, rare (1-2 % of the (t, E))
                     ESQ_STAT(E, 7, 1);
-                    if (m > ESQ_BUF) {  // re-flag (the compaction buffer was too small)
-                        pm0 = pm1 = 0u;
-#pragma unroll
-                        for (int c = 0; c < NC / 2; ++c) {
-                            if (D[c].x <= T) { if (2 * c < 32) pm0 |= 1u << (2 * c); else pm1 |= 1u << (2 * c - 32); }
-                            if (D[c].y <= T) { if (2 * c + 1 < 32) pm0 |= 1u << (2 * c + 1); else pm1 |= 1u << (2 * c + 1 - 32); }
-                        }
-                    }
-                    int ecnt = 0;
-                    for (int b0 = 0; (m > ESQ_BUF) ? __any_sync(FULL, (pm0 | pm1) != 0u) : b0 < m; b0 += 32) {
-                        bool act;
-                        int s = 0;
-                        if (m > ESQ_BUF) {
-                            act = (pm0 | pm1) != 0u;
-                            if (act) {
-                                int bb;
-                                if (pm0) { bb = __ffs(pm0) - 1; pm0 &= pm0 - 1; }
-                                else { bb = 32 + __ffs(pm1) - 1; pm1 &= pm1 - 1; }
-                                s = esq_label(lane, bb);
-                            }
-                        } else {
-                            act = b0 + lane < m;
-                            if (act) s = W.buf[b0 + lane];
-                        }
-                        const double Dx = act ? esq_exact(qaf, cbf, t, s, E, tau) : CUDART_INF;
-                        ecnt = esq_merge(W, ecnt, K, act, Dx, s, lane);
-                    }
-                    cnt = ecnt;
+                    cnt = esq_exact_select(W, qaf, cbf, t, E, tau, K, m, pm0, pm1, lane);
                     if (lane < cnt) {
                         exD = W.sD[lane];
                         ks = W.sS[lane];
