@@ -344,13 +344,16 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
             // the k-th smallest of >= k carried seeds is at most their max; S1 seeds at or above it
             // cannot lower the k-th smallest of the union and are dropped
             const unsigned thA = nA >= k ? __reduce_max_sync(FULL, kA) : 0xffffffffu;
+            int sB = -1;              // this lane's successor seed (label, fp32 value): also the
+            float fB = CUDART_INF_F;  // first fillers of the carried set if it comes out short
             if (e > 0 && e < prevEq && lane < K) {
                 const int l = W.lab[esq_loff(e) + lane];
                 const int s = l + 1;
                 if (l >= 0 && s < ncand && s - e * tau >= 0 && !(excl && s == t) &&
                     (W.tag[s] >> 5) != stamp) {  // not already a carried seed
-                    const float u = esq_upper(f32(t, s, E));
-                    const unsigned kv = __float_as_uint(u) + 1u;
+                    fB = f32(t, s, E);
+                    sB = s;
+                    const unsigned kv = __float_as_uint(esq_upper(fB)) + 1u;
                     if (kv < thA) kB = kv;
                 }
             }
@@ -488,6 +491,19 @@ __device__ __forceinline__ void esq_warp(const KnnParams& P, EsqWarp& W, const f
             const int nsel = cnt;  // >= k whenever the threshold is sound
             // fewer than K (tight threshold): complete the carried set with the lowest valid labels
             // not in it, so that the seeds at E+1 can still bound the k-th distance
+            if (cnt < K) {
+                // first the successor seeds that were not flagged (distinct from the set, value known)
+                const bool okB = sB >= 0 && fB > T;
+                const unsigned bm = __ballot_sync(FULL, okB);
+                const int rb = cnt + __popc(bm & ((1u << lane) - 1u));
+                __syncwarp();
+                if (okB && rb < K) { W.fbuf[rb] = fB; W.buf[rb] = (unsigned short)sB; }
+                __syncwarp();
+                const int addB = min(__popc(bm), K - cnt);
+                if (lane >= cnt && lane < cnt + addB) { kv = __float_as_uint(W.fbuf[lane]); ks = W.buf[lane]; }
+                __syncwarp();
+                cnt += addB;
+            }
             if (cnt < K) {
                 const int lo = E * tau;  // valid at E+1 as well
                 const int sf = lo + lane;

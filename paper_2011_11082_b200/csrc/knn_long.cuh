@@ -32,14 +32,18 @@ struct LngWarp {
     unsigned short buf[ESQ_BUF];   // compacted flagged labels
 };
 
-// Sorted order of the candidate values of every slot (E = 1 seeds): slab[b][i] = label of the
-// i-th smallest (value, label), pos[b][label] = i. One CTA of 512 threads per slot, bitonic sort
-// of (order-preserving value bits << 32 | label) keys in shared memory (dynamic: P2 * 8 bytes).
-__global__ void sort_series_kernel(const float* __restrict__ Xpad, int64_t ldpad, int padl, int ncand, int P2,
-                                   unsigned short* __restrict__ slab, unsigned short* __restrict__ pos, int64_t lds) {
+// Sorted order of the candidate values of every slot (the E-sequential kernels' E = 1 seeds):
+// slab[b][i] = label of the i-th smallest (value, label), pos[b][label] = i, for the candidates
+// x[0..ncand) of slot b's series (X row slot_series[b] or b; the sweep rescaling is a positive power
+// of two, so the order of the raw values is the order the kernels see). One CTA of 512 threads per
+// slot, bitonic sort of (order-preserving value bits << 32 | label) keys in shared memory
+// (dynamic: P2 * 8 bytes).
+__global__ void sort_series_kernel(const float* __restrict__ X, int64_t ldx, const int* __restrict__ slot_series,
+                                   int ncand, int P2, unsigned short* __restrict__ slab, unsigned short* __restrict__ pos,
+                                   int64_t lds) {
     extern __shared__ unsigned long long skeys[];
     const int b = blockIdx.x;
-    const float* x = Xpad + (int64_t)b * ldpad + padl;
+    const float* x = X + (int64_t)(slot_series ? slot_series[b] : b) * ldx;
     for (int i = threadIdx.x; i < P2; i += blockDim.x)
         skeys[i] = i < ncand ? ((unsigned long long)f32_order(x[i]) << 32) | (unsigned)i : ~0ull;
     __syncthreads();

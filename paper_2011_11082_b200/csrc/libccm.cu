@@ -330,13 +330,13 @@ edm_status launch_long_t(const KnnParams& P, dim3 grid, cudaStream_t st) {
     return EDM_OK;
 }
 // the sorted candidate order of every slot of a block (knn_long_kernel's E = 1 seeds)
-edm_status sort_series(const float* Xpad, int64_t ldpad, int tau, int ncand, int nslots, unsigned short* slab,
+edm_status sort_series(const float* X, int64_t ldx, const int* slot_series, int ncand, int nslots, unsigned short* slab,
                        unsigned short* pos, int64_t lds, cudaStream_t cs) {
     int P2 = 32;
     while (P2 < ncand) P2 <<= 1;
     const size_t smem = (size_t)P2 * 8;
-    CUDA_TRY(cudaFuncSetAttribute(sort_series_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    PROF_LAUNCH(EDM_PROF_PREP, cs, sort_series_kernel<<<nslots, 512, smem, cs>>>(Xpad, ldpad, knn_padl(tau), ncand, P2, slab, pos, lds));
+    if (smem > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(sort_series_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PROF_LAUNCH(EDM_PROF_PREP, cs, sort_series_kernel<<<nslots, 512, smem, cs>>>(X, ldx, slot_series, ncand, P2, slab, pos, lds));
     LAUNCH_CHECK("sort_series_kernel");
     return EDM_OK;
 }
@@ -592,12 +592,12 @@ edm_status edm_simplex_optimal_E(edm_dataset ds, int32_t E_max, int32_t tau, int
                 st = pad_series(W.Xs, L, nullptr, P.sexp, L, tau, nb, W.Xpad, cs);
                 if (st != EDM_OK) return st;
                 P.Xpad = W.Xpad; P.ldpad = knn_ldpad(L, tau);
-                const int ncand1 = (L + 1) / 2 - 1;
-                if (ncand1 > 32 * ESQ_NCMAX && ncand1 <= LNG_SORT_MAX) {
-                    st = sort_series(W.Xpad, P.ldpad, tau, ncand1, nb, W.lslab, W.lpos, W.llds, cs);
-                    if (st != EDM_OK) return st;
-                    P.lng_slab = W.lslab; P.lng_pos = W.lpos; P.lng_lds = W.llds;
-                }
+            }
+            const int ncand1 = (L + 1) / 2 - 1;
+            if (ncand1 > 32 * ESQ_NCMAX && ncand1 <= LNG_SORT_MAX) {  // knn_long_kernel's E = 1 seeds
+                st = sort_series(W.Xs, L, nullptr, ncand1, nb, W.lslab, W.lpos, W.llds, cs);
+                if (st != EDM_OK) return st;
+                P.lng_slab = W.lslab; P.lng_pos = W.lpos; P.lng_lds = W.llds;
             }
             st = launch_knn<MODE_SIMPLEX>(P, std::max(Ltgt - 1, 1), nb, cs);
             if (st != EDM_OK) return st;
@@ -890,12 +890,12 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
             st = pad_series(P.X, P.ldx, P.slot_series, P.sexp, Lk, tau, nb, W.Xpad, cs);
             if (st != EDM_OK) return st;
             P.Xpad = W.Xpad; P.ldpad = knn_ldpad(Lk, tau);
-            const int ncand2 = Lk - m_hi;
-            if (ncand2 > 32 * ESQ_NCMAX && ncand2 <= LNG_SORT_MAX && !P.slotE) {
-                st = sort_series(W.Xpad, P.ldpad, tau, ncand2, nb, W.lslab, W.lpos, W.llds, cs);
-                if (st != EDM_OK) return st;
-                P.lng_slab = W.lslab; P.lng_pos = W.lpos; P.lng_lds = W.llds;
-            }
+        }
+        const int ncand2 = Lk - m_hi;
+        if (ncand2 > 32 * ESQ_NCMAX && ncand2 <= LNG_SORT_MAX && !P.slotE && gser) {  // knn_long_kernel's E = 1 seeds
+            st = sort_series(P.X, P.ldx, P.slot_series, ncand2, nb, W.lslab, W.lpos, W.llds, cs);
+            if (st != EDM_OK) return st;
+            P.lng_slab = W.lslab; P.lng_pos = W.lpos; P.lng_lds = W.llds;
         }
         st = launch_knn<MODE_CCM>(P, Lk - m_hi, nb, cs);
         if (st != EDM_OK) return st;
