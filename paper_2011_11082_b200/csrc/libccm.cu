@@ -286,8 +286,13 @@ edm_status launch_knn_m(const KnnParams& P, dim3 grid, size_t smem, bool full, c
 // E-sequential kNN (knn_eseq.cuh): used when every E in 1..Etop is selected (target mode,
 // phase 1), the candidates fit the register chunks (ncand <= 32 ESQ_NCMAX) and no candidate
 // mask / global series copy is involved; CCM_KNN_ALGO=sweep forces knn_kernel (measurements).
+// queries per warp of the E-sequential kernel (longer runs amortise the run's first query, whose
+// threshold has no successor seeds; measured on c3: 48 for phase 2, 24 for phase 1)
 #ifndef CCM_ESQ_QPW
-#define CCM_ESQ_QPW 32
+#define CCM_ESQ_QPW 48
+#endif
+#ifndef CCM_ESQ_QPW1
+#define CCM_ESQ_QPW1 24
 #endif
 template <int MODE, bool TAU1, int NC>
 edm_status launch_esq_t(const KnnParams& P, dim3 grid, cudaStream_t st) {
@@ -361,7 +366,8 @@ edm_status launch_knn(const KnnParams& P0, int nq, int slots, cudaStream_t st) {
         }
         if (esq_eligible<MODE>(P, full, ncand)) {
             const char* qenv = getenv("CCM_ESQ_QPW");
-            const int qmax = std::min(ESQ_QPW_MAX, qenv ? std::max(1, atoi(qenv)) : CCM_ESQ_QPW);
+            const int qmax = std::min(ESQ_QPW_MAX, qenv ? std::max(1, atoi(qenv))
+                                                        : (MODE == MODE_SIMPLEX ? CCM_ESQ_QPW1 : CCM_ESQ_QPW));
             const int nc = std::max(1, (nq + ESQ_WARPS * qmax - 1) / (ESQ_WARPS * qmax));
             P.qpw = std::max(1, (nq + nc * ESQ_WARPS - 1) / (nc * ESQ_WARPS));
             dim3 g((nq + ESQ_WARPS * P.qpw - 1) / (ESQ_WARPS * P.qpw), slots);
