@@ -851,7 +851,7 @@ struct LookupParams {
 #define CCM_LK_STAGES 2
 #endif
 #ifndef CCM_LK_UNROLL
-#define CCM_LK_UNROLL 2
+#define CCM_LK_UNROLL 4
 #endif
 constexpr int LK_CHUNK = CCM_LK_CHUNK;    // bytes per stage
 constexpr int LK_STAGES = CCM_LK_STAGES;
