@@ -30,8 +30,8 @@
  *  - Indices are 0-based. Time labels: an embedded point is labelled by its
  *    latest time t, p(t) = (x[t], x[t-tau], ..., x[t-(E-1)tau]).
  *  - Undefined skill (a constant target) is a quiet NaN, never an error.
- *  - No global mutable state except the thread-local last-error string; reentrant on
- *    distinct streams and workspaces; deterministic (bit-identical reruns, and rho is
+ *  - No global mutable state except the thread-local last-error string and the device-memory
+ *    pool of edm_causal_map_host (mutex-protected); reentrant on distinct streams and workspaces; deterministic (bit-identical reruns, and rho is
  *    independent of how library rows are split across calls or GPUs).
  *  - Requires an sm_100 device (B200); otherwise EDM_EUNSUPPORTED.
  *  - Limits of this build: 1 <= E <= EDM_E_CAP (20, the paper's "<= 20 in practice",
@@ -213,12 +213,17 @@ size_t edm_workspace_bytes(int32_t which, int32_t N, int32_t L, int32_t E_max, i
  * over all series, then phase 2 over all library rows, and copies the results back.
  *   host_optE : int32[N] or NULL;  host_rho : float[N * N] (row = library);
  *   host_rhoE : float[N * E_max] or NULL.
- * Blocking; allocates and frees its own device memory. When host_rho is page-locked the map
+ * Blocking. Its device buffers come from a library-owned stream-ordered memory pool per device
+ * that keeps the memory between calls (repeated maps skip cudaMalloc/cudaFree of ~N^2 x 4 bytes);
+ * edm_release_cached_memory() returns it to the device. When host_rho is page-locked the map
  * is computed in 8 row chunks and each chunk's rows are copied back on a second stream while
  * the next chunk computes. Same errors as above. */
 edm_status edm_causal_map_host(const float *host_data, int32_t N, int32_t L, int32_t E_max,
                                int32_t tau, int32_t Tp, edm_e_mode mode, int32_t exclude_self,
                                int32_t *host_optE, float *host_rho, float *host_rhoE);
+
+/* Releases the device memory edm_causal_map_host keeps cached between calls (all devices). */
+edm_status edm_release_cached_memory(void);
 
 /* Thread-local message describing the last non-OK status returned on this thread. */
 const char *edm_last_error(void);

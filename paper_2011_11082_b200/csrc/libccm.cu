@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1066,6 +1067,39 @@ edm_status edm_ccm_tables(edm_dataset ds, const int32_t* E, int32_t tau, int32_t
                     ws_bytes, need, (cudaStream_t)stream, &cv, &to);
 }
 
+}  // extern "C"
+
+namespace {
+// edm_causal_map_host's device buffers come from one library-owned stream-ordered pool per device
+// that keeps its memory between calls (release threshold: unlimited), so repeated end-to-end maps
+// do not pay cudaMalloc / cudaFree of ~N^2 x 4 bytes each time; edm_release_cached_memory trims it.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[64] = {};
+cudaMemPool_t host_api_pool(int dev) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!g_pool[dev]) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&g_pool[dev], &props) != cudaSuccess) { g_pool[dev] = nullptr; return nullptr; }
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    return g_pool[dev];
+}
+}  // namespace
+
+extern "C" {
+
+edm_status edm_release_cached_memory(void) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (int d = 0; d < 64; ++d)
+        if (g_pool[d]) CUDA_TRY(cudaMemPoolTrimTo(g_pool[d], 0));
+    return EDM_OK;
+}
+
 edm_status edm_causal_map_host(const float* host_data, int32_t N, int32_t L, int32_t E_max, int32_t tau, int32_t Tp,
                                edm_e_mode mode, int32_t exclude_self, int32_t* host_optE, float* host_rho,
                                float* host_rhoE) {
@@ -1085,19 +1119,31 @@ edm_status edm_causal_map_host(const float* host_data, int32_t N, int32_t L, int
     int32_t* d_E = nullptr;
     void* ws = nullptr;
     std::vector<cudaEvent_t> evs;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool = host_api_pool(dev);
+    auto dalloc = [&](void** p, size_t bytes) {
+        return pool ? cudaMallocFromPoolAsync(p, bytes, pool, cs) : cudaMalloc(p, bytes);
+    };
+    auto dfree = [&](void* p) {
+        if (!p) return;
+        if (pool) cudaFreeAsync(p, cs);
+        else cudaFree(p);
+    };
     auto cleanup = [&]() {
         cudaStreamSynchronize(cs2);
         for (cudaEvent_t e : evs) cudaEventDestroy(e);
-        cudaFree(d_data); cudaFree(d_rho); cudaFree(d_rhoE); cudaFree(d_E); cudaFree(ws);
+        dfree(d_data); dfree(d_rho); dfree(d_rhoE); dfree(d_E); dfree(ws);
+        cudaStreamSynchronize(cs);
         cudaStreamDestroy(cs);
         cudaStreamDestroy(cs2);
     };
     auto run = [&]() -> edm_status {
-        CUDA_TRY(cudaMalloc(&d_data, sizeof(float) * (size_t)N * L));
-        CUDA_TRY(cudaMalloc(&d_rho, sizeof(float) * (size_t)N * N));
-        CUDA_TRY(cudaMalloc(&d_E, sizeof(int32_t) * N));
-        if (host_rhoE) CUDA_TRY(cudaMalloc(&d_rhoE, sizeof(float) * (size_t)N * E_max));
-        CUDA_TRY(cudaMalloc(&ws, std::max(ws0, ws1)));
+        CUDA_TRY(dalloc((void**)&d_data, sizeof(float) * (size_t)N * L));
+        CUDA_TRY(dalloc((void**)&d_rho, sizeof(float) * (size_t)N * N));
+        CUDA_TRY(dalloc((void**)&d_E, sizeof(int32_t) * N));
+        if (host_rhoE) CUDA_TRY(dalloc((void**)&d_rhoE, sizeof(float) * (size_t)N * E_max));
+        CUDA_TRY(dalloc(&ws, std::max(ws0, ws1)));
         CUDA_TRY(cudaMemcpyAsync(d_data, host_data, sizeof(float) * (size_t)N * L, cudaMemcpyHostToDevice, cs));
         edm_dataset ds{d_data, N, L, N};
         edm_status s = edm_simplex_optimal_E(ds, E_max, tau, 0, N, d_E, d_rhoE, ws, std::max(ws0, ws1), cs);

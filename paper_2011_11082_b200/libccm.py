@@ -33,7 +33,8 @@ E_CAP = 20
 EXPORTS = ("edm_embed_knn", "edm_simplex_optimal_E", "edm_ccm_all_pairs", "edm_workspace_bytes",
            "edm_causal_map_host", "edm_last_error", "edm_version", "edm_profile_begin", "edm_profile_end",
            "edm_ccm_lagged", "edm_ccm_lagged_workspace_bytes", "edm_ccm_convergence",
-           "edm_ccm_convergence_workspace_bytes", "edm_ccm_tables", "edm_ccm_tables_workspace_bytes", "edm_ccm_rows")
+           "edm_ccm_convergence_workspace_bytes", "edm_ccm_tables", "edm_ccm_tables_workspace_bytes", "edm_ccm_rows",
+           "edm_release_cached_memory")
 PROF_KINDS = ("prep", "simplex_knn", "simplex_rho", "ccm_knn", "lookup", "other")
 
 
@@ -83,6 +84,8 @@ def load(path: Optional[str] = None):
                                         sz, vp]
     lib.edm_ccm_convergence_workspace_bytes.restype = sz
     lib.edm_ccm_convergence_workspace_bytes.argtypes = [i32, i32, i32, i32, i32, i32]
+    lib.edm_release_cached_memory.restype = i32
+    lib.edm_release_cached_memory.argtypes = []
     lib.edm_ccm_rows.restype = i32
     lib.edm_ccm_rows.argtypes = [edm_dataset, vp, i32, i32, i32, i32, vp, i32, vp, vp, sz, vp]
     lib.edm_ccm_tables.restype = i32
@@ -147,7 +150,10 @@ def workspace(which: int, N: int, L: int, E_max: int, tau: int, Tp: int, device)
 
 
 def release_workspaces():
+    """Drop the cached workspaces and the device memory edm_causal_map_host keeps between calls."""
     _ws_cache.clear()
+    if _lib is not None:
+        _check(_lib.edm_release_cached_memory())
 
 
 def embed_knn(series: torch.Tensor, E: int, tau: int = 1, Tp: int = 1, exclude_self: bool = True,
