@@ -6,9 +6,12 @@
 //                         sweep exponent, fp64 mean and target exponent
 //   permute_kernel        centred, E-sorted, tile-padded time-major copy Yp     (S5)
 //   stats_kernel          per (E, column) fp64 sums of the observed window      (S5)
-//   knn_kernel<MODE>      fp64 incremental-over-E distances + warp top-(E+1)   (S1/S6/S7/S8)
+//   knn_kernel<MODE>      sweep kNN: fp32 prefilter of all E per candidate chunk, exact fp64
+//                         merges into per-E top-(E+1) lists (S1/S6/S7/S8): library mode,
+//                         convergence sets, very long series, edm_embed_knn
 //                         MODE_CCM: fused weights -> table; MODE_SIMPLEX: forecast;
 //                         MODE_EMBED: idx/dist/w of edm_embed_knn
+//   (knn_eseq.cuh / knn_long.cuh: the E-sequential kNN of phase 1 and target-mode phase 2)
 //   simplex_rho_kernel    two-pass fp64 Pearson of the phase-1 forecasts        (S2)
 //   argmax_kernel         optE = argmax_E rho(E)                                (S3)
 //   lookup_kernel<TILE>   gather-weighted lookup + fused Pearson moments        (S9)
