@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--N", type=int, default=None, help="override N (smaller runs of the same recipe)")
     ap.add_argument("--L", type=int, default=None, help="override L (long-series runs of the same recipe)")
     ap.add_argument("--mode", default="target", choices=["target", "library"])
+    ap.add_argument("--lookup", default="fp32", choices=["fp32", "u16"],
+                    help="u16: the opt-in 16-bit lookup targets (EDM_LOOKUP_U16, a separate line; the headline is fp32)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=None, help="oracle sample size (library rows)")
@@ -417,15 +419,16 @@ def main():
         if ev:
             ev[2].record(stream)
         if lags:
-            libccm.ccm_lagged(data, E, tau, lags[0], lags[1], args.mode, True, l0, l1, out=rho_rows)  # f1
+            libccm.ccm_lagged(data, E, tau, lags[0], lags[1], args.mode, True, l0, l1, out=rho_rows,
+                              lookup=args.lookup)  # f1
         elif conv:
             libccm.ccm_convergence(data, E, conv[0], conv[1], tau, Tp, args.mode, True, l0, l1)  # f2
         elif args.mode == "library" and world > 1:
             # library mode: rows dealt round-robin over the E-sorted order
             rows = distributed.assign_rows(E, world, "library")[rank]
-            libccm.ccm_rows(data, E, rows, tau, Tp, "library", True, out=rho_rows)  # S5-S9
+            libccm.ccm_rows(data, E, rows, tau, Tp, "library", True, out=rho_rows, lookup=args.lookup)  # S5-S9
         else:
-            libccm.ccm_all_pairs(data, E, tau, Tp, args.mode, True, l0, l1, out=rho_rows)  # S5-S9
+            libccm.ccm_all_pairs(data, E, tau, Tp, args.mode, True, l0, l1, out=rho_rows, lookup=args.lookup)  # S5-S9
         if ev:
             ev[3].record(stream)
         if world > 1:
@@ -510,11 +513,14 @@ def main():
                        "MEASURED_PEAKS.json has no smem figure -- the measured one is peak_measured)",
         "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_s * 1e3, "launches": lk_n,
         "share_of_step": lk_ms / ms_local if ms_local else None,
-        "pipe_model": {"frac": (lookup_pipe_cycles(E_host, L, tau, Tp, args.mode) * rows_frac * nlag * args.steps /
+        "pipe_model": {"frac": (lookup_pipe_cycles(E_host, L, tau, Tp, args.mode) * (0.5 if args.lookup == "u16" else 1.0)
+                                * rows_frac * nlag * args.steps /
                                 (nsm * sm_max_mhz * 1e6) / (lk_ms / 1e3)) if (lk_n and not conv) else None,
                        "note": "ideal shared-memory-pipe time of this instruction mix (per row: k gathers x 1 clk "
                                "+ ceil(k/2) uniform 16-B table broadcasts x 2 clk + 1 observation x 1 clk, costs from "
-                               "tools/shfl_bench.cu) / measured lookup time"},
+                               "tools/shfl_bench.cu) / measured lookup time" + ("; --lookup u16: the same per-row pipe "
+                               "cost serves 64 targets (two 16-bit codes per gathered word), so half the fp32 model's "
+                               "cycles" if args.lookup == "u16" else "")},
         "hbm_view": {"bound": "hbm", "target_tile_bytes_per_launch": ntiles_bytes,
                      "achieved": ntiles_bytes / avg_launch_s / 1e9 if lk_n else None, "peak": hbm_peak,
                      "frac": (ntiles_bytes / avg_launch_s / 1e9 / hbm_peak) if lk_n else None,
@@ -572,11 +578,11 @@ def main():
             host_np = host_pinned.numpy()
             libccm.release_workspaces()
             torch.cuda.empty_cache()
-            libccm.causal_map_host(host_np, E_max, tau, Tp, args.mode, True, rho_out=rho_host)  # warm
+            libccm.causal_map_host(host_np, E_max, tau, Tp, args.mode, True, rho_out=rho_host, lookup=args.lookup)  # warm
             ts = []
             for _ in range(args.e2e_steps):
                 t0 = time.perf_counter()
-                libccm.causal_map_host(host_np, E_max, tau, Tp, args.mode, True, rho_out=rho_host)
+                libccm.causal_map_host(host_np, E_max, tau, Tp, args.mode, True, rho_out=rho_host, lookup=args.lookup)
                 ts.append(time.perf_counter() - t0)
             sec = float(np.mean(ts))  # mean over the timed calls, like ms_per_step (total / K)
         else:
@@ -587,7 +593,8 @@ def main():
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 d = host_pinned.to(dev, non_blocking=True)
-                distributed.causal_map_distributed_to_host(d, rho_host, E_max, tau, Tp, args.mode, True)
+                distributed.causal_map_distributed_to_host(d, rho_host, E_max, tau, Tp, args.mode, True,
+                                                           lookup=args.lookup)
                 torch.cuda.synchronize()
                 el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
                 dist.all_reduce(el, op=dist.ReduceOp.MAX)
@@ -628,9 +635,12 @@ def main():
             "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": vs_base, "vs_baseline_ref": PAPER_C3_REF if vs_base else None,
-            "dtype": "f32 kNN certified against f64 keys / f32 lookup", "data": "synthetic",
+            "dtype": "f32 kNN certified against f64 keys / " + ("u16-code lookup (EDM_LOOKUP_U16, fp32 arithmetic)"
+                                                                   if args.lookup == "u16" else "f32 lookup"),
+            "data": "synthetic",
             "config": {"workload": f"{args.config}: {N} series x L={L}, E=1..{E_max}, tau={tau}, Tp={Tp}, "
-                                   f"mode={args.mode}, exclude_self", "N": N, "L": L,
+                                   f"mode={args.mode}, exclude_self" + (", lookup=u16" if args.lookup == "u16" else ""),
+                       "N": N, "L": L, "lookup": args.lookup,
                        "parallelism": f"library rows / series sharded over {world} GPU(s)",
                        "l2": "inputs larger than L2 (dataset %.0f MB, tables+tiles stream through L2)" % (N * L * 4 / 1e6)},
             "phase_ms_per_step": {"simplex": phases[0] / args.steps, "allgather_E": phases[1] / args.steps,

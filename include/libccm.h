@@ -63,6 +63,18 @@ typedef enum {
     EDM_E_LIBRARY = 1 /* north_star wording: the table is built at optE[library] */
 } edm_e_mode;
 
+/* Opt-in precision variant of the lookup (S9), OR-ed into `mode` of edm_ccm_all_pairs,
+ * edm_ccm_rows, edm_ccm_lagged and edm_causal_map_host (other calls: EINVAL). Not a paper step
+ * (the paper's lookup is the plain weighted sum): every centred target series is
+ * mapped affinely onto 16-bit codes u = rint((y - min) * 65535 / (max - min)) and the lookup
+ * gathers two targets per 32-bit shared-memory word (64-target tiles). Pearson rho is
+ * invariant under the affine map, so only the rounding perturbs it (|drho| below 1e-4 on the
+ * tests' workloads); a 64-target tile runs on the fp32 path whenever one of its
+ * targets has an observed window whose standard deviation is below range / 16, or whose codes
+ * are constant while its values are not. kNN tables and optE are unaffected (bit-exact).
+ * Ignored (fp32 lookup) when the fp32 tile does not fit shared memory (L above about 1,600). */
+#define EDM_LOOKUP_U16 0x100
+
 /* A float32 dataset in device memory, time-major: value of series j at time t is
  * data[t * ld + j], 0 <= t < L, 0 <= j < N, ld >= N ("an L x N array ts"). */
 typedef struct {

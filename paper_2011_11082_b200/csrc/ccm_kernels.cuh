@@ -174,34 +174,92 @@ __global__ void permute_kernel(const float* __restrict__ y, int64_t ld, int L, i
 // the same for every E). stats[(E-1)*Np + p] = (sum y, sum y^2) of the centred fp32 column
 // over it (fp64), cflag[(E-1)*Np + p] = 1 if every raw value in it is equal (NaN skill).
 // Single-horizon CCM: d = Tp, obs_end = L-1; time-delay cross map: d = m_lo + lag.
+// ---- 16-bit lookup targets (EDM_LOOKUP_U16, an opt-in precision variant of S9):
+// every centred target column p is mapped affinely onto [0.5, 2 - 2^-15],
+// a = 0.5 + (v - min) (1.5 - 2^-15) / (max - min) over its whole series, and rounded to the
+// nearest float with 16 significant bits (steps 2^-16 below 1, 2^-15 above); the code is bits
+// 23..8 of that float (exponent LSB + 15 mantissa bits), so that the lookup rebuilds the value
+// with one byte permute (bytes 0x3F, code, 0x00). Codes are stored in 64-column [L][64] tiles
+// (yq_index): one conflict-free 32-bit shared-memory gather serves two targets. Pearson rho is
+// invariant under the affine map (of predictions and observations alike), so only the
+// rounding perturbs it; stats_kernel flags every 64-tile whose rounding could matter (qbad) and
+// the lookup runs those tiles on the fp32 path.
+constexpr int TILE_Q = 64;
+__host__ __device__ __forceinline__ int64_t yq_index(int p, int t, int L) {
+    return ((int64_t)(p >> 6) * L + t) * 64 + (p & 63);
+}
+__global__ void quantize_kernel(const float* __restrict__ Yp, int L, int Np, unsigned short* __restrict__ Yq,
+                                float* __restrict__ qrange) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= Np) return;
+    float mn = CUDART_INF_F, mx = -CUDART_INF_F;
+    for (int t = 0; t < L; ++t) {
+        const float v = Yp[yp_index(p, t, L)];
+        mn = fminf(mn, v);
+        mx = fmaxf(mx, v);
+    }
+    const double span = (double)mx - (double)mn;
+    const double sc = span > 0.0 ? (1.5 - 0x1p-15) / span : 0.0;
+    for (int t = 0; t < L; ++t) {
+        const double a = fmin(fmax(0.5 + ((double)Yp[yp_index(p, t, L)] - (double)mn) * sc, 0.5), 2.0 - 0x1p-15);
+        const double q = a < 1.0 ? rint(a * 65536.0) * 0x1p-16 : rint(a * 32768.0) * 0x1p-15;  // exact in fp32
+        Yq[yq_index(p, t, L)] = (unsigned short)((__float_as_uint((float)q) >> 8) & 0xFFFFu);
+    }
+    qrange[p] = (float)span;
+}
+
+// The value of a 16-bit code (quantize_kernel): the float with bytes (0x3F, code, 0x00).
+__device__ __forceinline__ float q_value(unsigned short c) { return __uint_as_float(0x3F000000u | ((uint32_t)c << 8)); }
+// Optional (Yq != NULL, the 16-bit lookup): statsq = the same sums of the codes' values, and qbad[p / 64] |= 1 when the window is not constant but its 16-bit codes are,
+// or its range-to-deviation ratio range / sd exceeds sqrt(qmax2) (the rounding's share of the
+// window's variance).
 __global__ void stats_kernel(const float* __restrict__ Yp, int L, const float* __restrict__ y, int64_t ld,
                              const int* __restrict__ colmap, int Np, int tau, int d, int obs_end, int Emax,
-                             double2* __restrict__ stats, int* __restrict__ cflag) {
+                             double2* __restrict__ stats, int* __restrict__ cflag,
+                             const unsigned short* __restrict__ Yq, const float* __restrict__ qrange,
+                             double2* __restrict__ statsq, int* __restrict__ qbad, double qmax2) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= Np) return;
     const int c = colmap[p];
-    double s1 = 0.0, s2 = 0.0;
-    bool same = true;
+    double s1 = 0.0, s2 = 0.0, q1 = 0.0, q2 = 0.0;
+    bool same = true, qsame = true;
     const float last = c >= 0 ? y[(int64_t)obs_end * ld + c] : 0.f;
+    const unsigned short qlast = Yq ? Yq[yq_index(p, obs_end, L)] : 0;
+    const double r2 = Yq ? (double)qrange[p] * (double)qrange[p] : 0.0;
     int e = Emax;  // next E to record, descending: start index (e-1)tau+d increases with e
     for (; e >= 1 && (e - 1) * tau + d > obs_end; --e) {  // empty window: infeasible E
         stats[(int64_t)(e - 1) * Np + p] = make_double2(0.0, 0.0);
         cflag[(int64_t)(e - 1) * Np + p] = 1;
+        if (Yq) statsq[(int64_t)(e - 1) * Np + p] = make_double2(0.0, 0.0);
     }
     for (int t = obs_end; t >= 0 && e >= 1; --t) {
         const double v = (double)Yp[yp_index(p, t, L)];
         s1 += v;
         s2 += v * v;
         if (c >= 0 && y[(int64_t)t * ld + c] != last) same = false;
+        if (Yq) {
+            const unsigned short uq = Yq[yq_index(p, t, L)];
+            const double u = (double)q_value(uq);
+            q1 += u;
+            q2 += u * u;
+            if (uq != qlast) qsame = false;
+        }
         while (e >= 1 && t == (e - 1) * tau + d) {
             stats[(int64_t)(e - 1) * Np + p] = make_double2(s1, s2);
             cflag[(int64_t)(e - 1) * Np + p] = same ? 1 : 0;
+            if (Yq) {
+                statsq[(int64_t)(e - 1) * Np + p] = make_double2(q1, q2);
+                const double n = (double)(obs_end - t + 1);
+                const double var = s2 / n - (s1 / n) * (s1 / n);
+                if (!same && (qsame || !(var > 0.0) || r2 > qmax2 * var)) atomicOr(qbad + (p >> 6), 1);
+            }
             --e;
         }
     }
     for (; e >= 1; --e) {
         stats[(int64_t)(e - 1) * Np + p] = make_double2(0.0, 0.0);
         cflag[(int64_t)(e - 1) * Np + p] = 1;
+        if (Yq) statsq[(int64_t)(e - 1) * Np + p] = make_double2(0.0, 0.0);
     }
 }
 
@@ -843,6 +901,10 @@ struct LookupParams {
     int Eok;                // E > Eok: no table (convergence test, library set too small) -> NaN
     int ntiles, nsplit;     // the last nsplit tiles run as `parts` CTAs each (library ranges)
     int parts;
+    // 16-bit lookup (lookup_kernel<true, true>): tiles are 64 targets (ntiles counts them)
+    const unsigned short* Yq;  // [Np/64][L][64] codes (yq_index)
+    const double2* statsq;     // [ECAP][Np] observed-window sums of u * 2^-23
+    const int* qbad;           // [Np/64] tile runs on the fp32 path
 };
 
 // ---- per-warp table staging: TMA bulk copies (cp.async.bulk) into a 2-stage shared-memory
@@ -983,6 +1045,129 @@ __device__ __forceinline__ void lookup_one(const LookupParams& P, const float* _
     }
 }
 
+// ---- the 16-bit variant: lane = targets 2 lane, 2 lane + 1 of a 64-target tile, whose codes share
+// one 32-bit word of the [L][64] tile row (128 B, the fp32 tile's row size: same gather addresses).
+// A code becomes its value in [0.5, 2) with one PRMT (q_value); both targets' products and
+// moments use packed fp32 (FFMA2 with the weight broadcast / FADD2).
+__device__ __forceinline__ unsigned long long lk_bits(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
+__device__ __forceinline__ float2 lk_f2(unsigned long long u) { return *reinterpret_cast<float2*>(&u); }
+__device__ __forceinline__ float2 lk_add2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(lk_bits(a)), "l"(lk_bits(b)));
+    return lk_f2(r);
+}
+__device__ __forceinline__ float2 lk_sub2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(lk_bits(a)), "l"(lk_bits(b)));
+    return lk_f2(r);
+}
+__device__ __forceinline__ float2 lk_fma2(float2 a, float2 b, float2 c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(lk_bits(a)), "l"(lk_bits(b)), "l"(lk_bits(c)));
+    return lk_f2(r);
+}
+__device__ __forceinline__ float2 lk_codes(uint32_t w) {
+    return make_float2(__uint_as_float(__byte_perm(w, 0x3F000000u, 0x7104)),
+                       __uint_as_float(__byte_perm(w, 0x3F000000u, 0x7324)));
+}
+
+template <int E>
+__device__ __forceinline__ void lookup_one_q(const LookupParams& P, const float* __restrict__ Y, int tile, int b,
+                                             int lane, int col0, int col1, WarpRing& R) {
+    constexpr int k = E + 1, kp = kpad(k);
+    constexpr int ROWS = LK_CHUNK / (8 * kp);
+    constexpr int CB = ROWS * kp * 8;
+    const char* tab = reinterpret_cast<const char*>(P.tables + (int64_t)b * P.T_lib + P.offE[E]);
+    const int t0 = (E - 1) * P.tau;
+    const int n = P.Lk - t0 - P.hrz;
+    const int nch = (n + ROWS - 1) / ROWS;
+    auto issue = [&](int ci, uint32_t slot) {
+        const int rows = min(ROWS, n - ci * ROWS);
+        tma_load_1d(R.buf + slot * (LK_CHUNK / 16), tab + (int64_t)ci * CB, (uint32_t)(rows * kp * 8), R.bar + slot);
+    };
+    if (lane == 0) {
+        fence_proxy_async();
+#pragma unroll
+        for (int i = 0; i < LK_STAGES; ++i)
+            if (i < nch) issue(i, (R.it + i) % LK_STAGES);
+    }
+    double Sp0 = 0.0, Spp0 = 0.0, Spo0 = 0.0, Sp1 = 0.0, Spp1 = 0.0, Spo1 = 0.0;
+    const uint32_t* Yo = reinterpret_cast<const uint32_t*>(Y) + (int64_t)(t0 + P.oshift) * TILE_J + lane;
+    const char* Yb = reinterpret_cast<const char*>(Y);
+    const uint32_t rowb = (uint32_t)(TILE_J * sizeof(uint32_t));
+    uint32_t lbase = (uint32_t)((P.gshift * TILE_J + lane) * sizeof(uint32_t));
+    asm("" : "+r"(lbase));
+    auto Yl = [&](uint32_t idx) { return lk_codes(*reinterpret_cast<const uint32_t*>(Yb + (idx * rowb + lbase))); };
+    float2 c = make_float2(0.f, 0.f);
+    for (int ci = 0; ci < nch; ++ci) {
+        const uint32_t slot = R.it % LK_STAGES;
+        mbar_wait(R.bar + slot, (R.it / LK_STAGES) & 1u);
+        const uint4* rowp = R.buf + slot * (LK_CHUNK / 16);
+        const int r0 = ci * ROWS, r1 = min(n, r0 + ROWS);
+        float2 sp = make_float2(0.f, 0.f), spp = sp, spo = sp;
+#pragma unroll LK_UNROLL
+        for (int r = r0; r < r1; ++r) {
+            const uint4* row = rowp + (r - r0) * (kp / 2);
+            float2 p = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int j2 = 0; j2 < kp / 2; ++j2) {
+                const uint4 e2 = row[j2];
+                CCM_CHECK((int)e2.x + P.gshift >= 0 && (int)e2.x + P.gshift < P.Lt);
+                CCM_CHECK(2 * j2 + 1 >= k || ((int)e2.z + P.gshift >= 0 && (int)e2.z + P.gshift < P.Lt));
+                const float w0 = __uint_as_float(e2.y);
+                p = lk_fma2(make_float2(w0, w0), Yl(e2.x), p);
+                if (2 * j2 + 1 < k) {
+                    const float w1 = __uint_as_float(e2.w);
+                    p = lk_fma2(make_float2(w1, w1), Yl(e2.z), p);
+                }
+            }
+            if (r == 0) c = p;
+            p = lk_sub2(p, c);
+            CCM_CHECK(t0 + P.oshift + r >= 0 && t0 + P.oshift + r < P.Lt);
+            const float2 o = lk_codes(Yo[(int64_t)r * TILE_J]);
+            sp = lk_add2(sp, p);
+            spp = lk_fma2(p, p, spp);
+            spo = lk_fma2(p, o, spo);
+        }
+        Sp0 += (double)sp.x; Spp0 += (double)spp.x; Spo0 += (double)spo.x;
+        Sp1 += (double)sp.y; Spp1 += (double)spp.y; Spo1 += (double)spo.y;
+        __syncwarp();
+        ++R.it;
+        if (lane == 0 && ci + LK_STAGES < nch) {
+            fence_proxy_async();
+            issue(ci + LK_STAGES, slot);
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int col = h ? col1 : col0;
+        if (col < 0) continue;
+        const int pcol = tile * TILE_Q + 2 * lane + h;
+        const double2 st = P.statsq[(int64_t)(E - 1) * P.Np + pcol];
+        const bool o_const = P.cflag[(int64_t)(E - 1) * P.Np + pcol] != 0;
+        const double nn = (double)n;
+        const double Sp = h ? Sp1 : Sp0, Spp = h ? Spp1 : Spp0, Spo = h ? Spo1 : Spo0;
+        const double cov = Spo - Sp * st.x / nn;
+        const double vp = Spp - Sp * Sp / nn;
+        const double vo = st.y - st.x * st.x / nn;
+        float r = CUDART_NAN_F;
+        if (!o_const && vp > 0.0 && vo > 0.0) r = (float)(cov / sqrt(vp * vo));
+        P.rho[((int64_t)P.slotRow[b] - P.rbase) * P.rstride + P.roff + col] = r;
+    }
+}
+
+__device__ __forceinline__ void lookup_dispatch_q(int E, const LookupParams& P, const float* Y, int tile, int b,
+                                                  int lane, int col0, int col1, WarpRing& R) {
+    switch (E) {
+#define CCM_CASE(e) case e: lookup_one_q<e>(P, Y, tile, b, lane, col0, col1, R); break;
+        CCM_CASE(1) CCM_CASE(2) CCM_CASE(3) CCM_CASE(4) CCM_CASE(5) CCM_CASE(6) CCM_CASE(7)
+        CCM_CASE(8) CCM_CASE(9) CCM_CASE(10) CCM_CASE(11) CCM_CASE(12) CCM_CASE(13) CCM_CASE(14)
+        CCM_CASE(15) CCM_CASE(16) CCM_CASE(17) CCM_CASE(18) CCM_CASE(19) CCM_CASE(20)
+#undef CCM_CASE
+        default: break;
+    }
+}
+
 __device__ __forceinline__ void lookup_dispatch(int E, const LookupParams& P, const float* Y, int64_t ys, int tile,
                                                 int b, int lane, int col, WarpRing& R) {
     switch (E) {
@@ -1004,8 +1189,9 @@ constexpr size_t lookup_ring_bytes() { return (size_t)LOOKUP_WARPS * LK_STAGES *
 // reuse); SMEM = false (long series): gathers straight from L2/HBM. Tiles run in reverse
 // order so that the expensive high-E tiles (target mode) start first.
 // Dynamic smem: [tile: L*32 floats if SMEM][ring: LOOKUP_WARPS*2*LK_CHUNK][bars].
-template <bool SMEM>
+template <bool SMEM, bool Q16>
 __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupParams P) {
+    static_assert(SMEM || !Q16, "the 16-bit lookup needs the shared-memory tile");
     extern __shared__ __align__(16) unsigned char lk_smem[];
     // CTAs 0 .. ntiles-nsplit-1 take whole tiles from the last (target mode: highest E, the
     // most expensive) down; the remaining nsplit cheapest tiles run as `parts` CTAs each, part p
@@ -1025,50 +1211,80 @@ __global__ void __launch_bounds__(LOOKUP_WARPS * 32, 1) lookup_kernel(LookupPara
         }
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int Et = P.tileE ? P.tileE[tile] : 0;
+    const int Et = P.tileE ? P.tileE[Q16 ? 2 * tile : tile] : 0;
     if (P.tileE && Et <= 0) return;
     float* ytile = reinterpret_cast<float*>(lk_smem);
     const size_t tile_bytes = SMEM ? (size_t)P.Lt * TILE_J * sizeof(float) : 0;
     uint4* ring = reinterpret_cast<uint4*>(lk_smem + tile_bytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(lk_smem + tile_bytes + (size_t)LOOKUP_WARPS * LK_STAGES * LK_CHUNK);
+    uint64_t* tbar = bars + LOOKUP_WARPS * LK_STAGES;
     WarpRing R{ring + (size_t)warp * LK_STAGES * (LK_CHUNK / 16), bars + warp * LK_STAGES, 0u};
     if (lane == 0) {
         for (int s = 0; s < LK_STAGES; ++s) mbar_init(R.bar + s, 1);
         fence_mbar_init();
     }
-    const float* Y;
-    int64_t ys;
-    const float* src = P.Yp + yp_index(tile * TILE_J, 0, P.Lt);  // the tile's contiguous [L][32] block
-    if (SMEM) {
-        // the tile's contiguous [L][32] block staged by TMA bulk copies (cp.async.bulk, 32 KB each)
-        // completing on one mbarrier; every thread waits on its phase 0
-        uint64_t* tbar = bars + LOOKUP_WARPS * LK_STAGES;
+    if (SMEM && threadIdx.x == 0) {
+        mbar_init(tbar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();  // the barriers' initialisation is visible before anyone uses them
+    // the tile's contiguous [L][32] fp32 (or [L][64] 16-bit) block, L * 128 bytes, staged by TMA
+    // bulk copies (cp.async.bulk, 32 KB each) completing on the tile barrier's phase `ph`
+    auto stage = [&](const void* src, uint32_t ph) {
         const uint32_t total = (uint32_t)P.Lt * TILE_J * sizeof(float);
         constexpr uint32_t TCH = 32768;
         if (threadIdx.x == 0) {
-            mbar_init(tbar, (total + TCH - 1) / TCH);
-            fence_mbar_init();
-            fence_proxy_async();
-            for (uint32_t off = 0; off < total; off += TCH)
-                tma_load_1d(reinterpret_cast<char*>(ytile) + off, reinterpret_cast<const char*>(src) + off,
-                            min(TCH, total - off), tbar);
+            fence_proxy_async();  // earlier generic reads of the tile (previous half) before the async writes
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(tbar)), "r"(total)
+                         : "memory");
+            for (uint32_t off = 0; off < total; off += TCH) {
+                const uint32_t nb = min(TCH, total - off);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(reinterpret_cast<char*>(ytile) + off)),
+                    "l"(reinterpret_cast<const char*>(src) + off), "r"(nb), "r"(smem_u32(tbar))
+                    : "memory");
+            }
         }
-        __syncthreads();  // the barrier's initialisation is visible before anyone waits on it
-        mbar_wait(tbar, 0u);
-        Y = ytile;
-    } else {
-        Y = src;  // gathers from L2/HBM; byte offsets idx * 128 + lane * 4 stay 32-bit (L < 2^25)
+        mbar_wait(tbar, ph);
+    };
+    if (Q16 && !P.qbad[tile]) {
+        stage(P.Yq + yq_index(tile * TILE_Q, 0, P.Lt), 0u);
+        const int col0 = P.colmap[tile * TILE_Q + 2 * lane], col1 = P.colmap[tile * TILE_Q + 2 * lane + 1];
+        for (int b = part * LOOKUP_WARPS + warp; b < P.B; b += parts * LOOKUP_WARPS) {
+            const int E = P.tileE ? Et : P.slotE[b];
+            if (E > P.Eok) {
+                const int64_t o = ((int64_t)P.slotRow[b] - P.rbase) * P.rstride + P.roff;
+                if (col0 >= 0) P.rho[o + col0] = CUDART_NAN_F;
+                if (col1 >= 0) P.rho[o + col1] = CUDART_NAN_F;
+                continue;
+            }
+            lookup_dispatch_q(E, P, ytile, tile, b, lane, col0, col1, R);
+        }
+        return;
     }
-    ys = TILE_J;
-    __syncthreads();
-    const int col = P.colmap[tile * TILE_J + lane];
-    for (int b = part * LOOKUP_WARPS + warp; b < P.B; b += parts * LOOKUP_WARPS) {
-        const int E = P.tileE ? Et : P.slotE[b];
-        if (E > P.Eok) {
-            if (col >= 0) P.rho[((int64_t)P.slotRow[b] - P.rbase) * P.rstride + P.roff + col] = CUDART_NAN_F;
-            continue;
+    // fp32 path: one 32-target tile, or (Q16, a flagged 64-tile) its two halves in turn
+#pragma unroll 1
+    for (int half = 0; half < (Q16 ? 2 : 1); ++half) {
+        const int t32 = Q16 ? 2 * tile + half : tile;
+        const float* src = P.Yp + yp_index(t32 * TILE_J, 0, P.Lt);
+        const float* Y;
+        if (SMEM) {
+            if (half) __syncthreads();  // every warp is done with the first half
+            stage(src, (uint32_t)half);
+            Y = ytile;
+        } else {
+            Y = src;  // gathers from L2/HBM; byte offsets idx * 128 + lane * 4 stay 32-bit (L < 2^25)
         }
-        lookup_dispatch(E, P, Y, ys, tile, b, lane, col, R);
+        const int col = P.colmap[t32 * TILE_J + lane];
+        for (int b = part * LOOKUP_WARPS + warp; b < P.B; b += parts * LOOKUP_WARPS) {
+            const int E = P.tileE ? Et : P.slotE[b];
+            if (E > P.Eok) {
+                if (col >= 0) P.rho[((int64_t)P.slotRow[b] - P.rbase) * P.rstride + P.roff + col] = CUDART_NAN_F;
+                continue;
+            }
+            lookup_dispatch(E, P, Y, TILE_J, t32, b, lane, col, R);
+        }
     }
 }
 

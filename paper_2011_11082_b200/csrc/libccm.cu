@@ -116,8 +116,22 @@ inline int ccm_block(int64_t T_lib) {
     return (int)std::max<int64_t>(LOOKUP_WARPS, std::min<int64_t>(CCM_B, fit / LOOKUP_WARPS * LOOKUP_WARPS));
 }
 constexpr int LOOKUP_SMEM_MAX = 227 * 1024;
+// 16-bit lookup guard: a 64-target tile runs on the fp32 path when one of its targets has an
+// observed window whose sd is below range / LOOKUP_Q_RMAX (range of the whole series), i.e. when
+// the 16-bit rounding (step range / 65535) exceeds 1 / (65535 / RMAX) of the window's sd
+// (measured error vs the ratio)
+#ifndef CCM_LOOKUP_Q_RMAX
+#define CCM_LOOKUP_Q_RMAX 16.0
+#endif
+constexpr double LOOKUP_Q_RMAX = CCM_LOOKUP_Q_RMAX;
+inline bool mode_ok(edm_e_mode m, bool allow_u16) {
+    int v = (int)m;
+    if (allow_u16) v &= ~EDM_LOOKUP_U16;
+    return v == EDM_E_TARGET || v == EDM_E_LIBRARY;
+}
 
-inline int64_t np_max(int N) { return (int64_t)(N + TILE_J - 1) / TILE_J * TILE_J + (int64_t)TILE_J * ECAP; }
+// permuted target columns: every E segment padded to 64 (the 16-bit lookup's tile; 32 for fp32)
+inline int64_t np_max(int N) { return (int64_t)(N + TILE_Q - 1) / TILE_Q * TILE_Q + (int64_t)TILE_Q * ECAP; }
 
 struct SimplexWs {
     int SB;         // series per phase-1 block: SIMPLEX_SLOTS, fewer when the lists exceed the budget
@@ -184,6 +198,10 @@ struct CcmWs {
     int* rsexp;         // [N] sweep exponent of library row r (list order)
     double2* stats;     // [nlag][ECAP][Npm] observed-window sums
     int* cflag;         // [nlag][ECAP][Npm] observed window constant
+    unsigned short* Yq; // [Npm/64][L][64] 16-bit target codes (EDM_LOOKUP_U16; yq_index)
+    float* qrange;      // [Npm] range of the centred column
+    double2* statsq;    // [nlag][ECAP][Npm] observed-window sums of the codes
+    int* qbad;          // [Npm/64] 64-tile runs on the fp32 path
     int* slot_series;   // [N]
     int* slot_row;      // [N]
     int* slotE;         // [N]
@@ -218,6 +236,10 @@ CcmWs ccm_ws(void* base, int N, int L, int Lk, int tau, int hrz, int nlag) {
     w.rsexp = (int*)take((size_t)N * sizeof(int));
     w.stats = (double2*)take((size_t)nlag * ECAP * w.Npm * sizeof(double2));
     w.cflag = (int*)take((size_t)nlag * ECAP * w.Npm * sizeof(int));
+    w.Yq = (unsigned short*)take((size_t)L * w.Npm * sizeof(unsigned short));
+    w.qrange = (float*)take((size_t)w.Npm * sizeof(float));
+    w.statsq = (double2*)take((size_t)nlag * ECAP * w.Npm * sizeof(double2));
+    w.qbad = (int*)take((size_t)(w.Npm / TILE_Q) * sizeof(int));
     w.slot_series = (int*)take((size_t)N * sizeof(int));
     w.slot_row = (int*)take((size_t)N * sizeof(int));
     w.slotE = (int*)take((size_t)N * sizeof(int));
@@ -727,8 +749,8 @@ edm_status conv_blocks(edm_dataset ds, const CcmWs& W, const int64_t offE[ECAP +
                 } else {
                     Q.rho = C.samples; Q.rstride = (int64_t)R * N; Q.roff = (int64_t)r * N; Q.rbase = r0;
                 }
-                if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
-                else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+                if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true, false><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+                else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false, false><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
                 LAUNCH_CHECK("lookup_kernel");
             }
             if (to) continue;
@@ -758,6 +780,9 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
     if (need == 0 || ws_bytes < need) return fail(EDM_EWORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
     edm_status st = check_device();
     if (st != EDM_OK) return st;
+    // EDM_LOOKUP_U16: 16-bit lookup targets (single map / lags with the shared-memory tile only)
+    bool q16 = ((int)mode & EDM_LOOKUP_U16) != 0 && !cv && !to;
+    mode = (edm_e_mode)((int)mode & ~EDM_LOOKUP_U16);
     const int N = ds.N, L = ds.L, Lk = L - m_lo, nlag = lag_max - lag_min + 1;
     CcmWs W = ccm_ws(workspace, N, L, Lk, tau, m_hi, nlag);
     char* extra = (char*)workspace + W.bytes;
@@ -792,7 +817,10 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
     table_layout(Lk, tau, m_hi, offE, &T_lib);
 
     // target ordering (S5): target mode -> stable counting sort by (E_j, j), every E segment
-    // padded to a multiple of 32 so that a 32-target tile has one E; library mode -> identity.
+    // padded to a multiple of 32 (64 for the 16-bit lookup) so that a tile has one E; library
+    // mode -> identity. tileE / Np count 32-target tiles either way.
+    q16 = q16 && (size_t)L * TILE_J * sizeof(float) + lookup_ring_bytes() <= (size_t)LOOKUP_SMEM_MAX;
+    const int G = q16 ? TILE_Q : TILE_J;
     std::vector<int> colmap, tileE;
     if (mode == EDM_E_TARGET) {
         std::vector<int> cnt(ECAP + 2, 0);
@@ -801,7 +829,7 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
         int64_t pos = 0;
         for (int e = 1; e <= ECAP; ++e) {
             seg[e] = (int)pos;
-            const int nt = (cnt[e] + TILE_J - 1) / TILE_J;
+            const int nt = (cnt[e] + G - 1) / G * (G / TILE_J);
             for (int t = 0; t < nt; ++t) tileE.push_back(e);
             pos += (int64_t)nt * TILE_J;
         }
@@ -809,13 +837,14 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
         std::vector<int> fill(seg);
         for (int j = 0; j < N; ++j) colmap[fill[hE[j]]++] = j;
     } else {
-        const int nt = (N + TILE_J - 1) / TILE_J;
+        const int nt = (N + G - 1) / G * (G / TILE_J);
         colmap.assign((size_t)nt * TILE_J, -1);
         for (int j = 0; j < N; ++j) colmap[j] = j;
         tileE.assign(nt, 0);
     }
     const int ntiles = (int)tileE.size();
     const int Np = ntiles * TILE_J;
+    const int ntl = q16 ? ntiles / 2 : ntiles;  // lookup tiles (64 targets each with q16)
     // library slots: row r of this call is series lib(r) = lib_list[r] (edm_ccm_rows) or lib_begin + r
     const int nlib = lib_end - lib_begin;
     auto lib = [&](int r) { return lib_list ? lib_list[r] : lib_begin + r; };
@@ -864,11 +893,18 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
             dim3 pg((Np + 255) / 256, std::min(L, 256));
             PROF_LAUNCH(EDM_PROF_PREP, cs, permute_kernel<<<pg, 256, 0, cs>>>(ds.data, ds.ld, L, Np, W.colmap, W.mean, W.texp, W.Yp));
             LAUNCH_CHECK("permute_kernel");
+            if (q16) {
+                PROF_LAUNCH(EDM_PROF_PREP, cs, quantize_kernel<<<(Np + 127) / 128, 128, 0, cs>>>(W.Yp, L, Np, W.Yq, W.qrange));
+                LAUNCH_CHECK("quantize_kernel");
+                CUDA_TRY(cudaMemsetAsync(W.qbad, 0, sizeof(int) * (size_t)ntl, cs));
+            }
             for (int l = lag_min; l <= lag_max; ++l) {
                 const int64_t so = (int64_t)(l - lag_min) * ECAP * W.Npm;
                 PROF_LAUNCH(EDM_PROF_PREP, cs,
                             stats_kernel<<<(Np + 127) / 128, 128, 0, cs>>>(W.Yp, L, ds.data, ds.ld, W.colmap, Np, tau, m_lo + l,
-                                                                          L - 1 - m_hi + l, ECAP, W.stats + so, W.cflag + so));
+                                                                          L - 1 - m_hi + l, ECAP, W.stats + so, W.cflag + so,
+                                                                          q16 ? W.Yq : nullptr, W.qrange, W.statsq + so,
+                                                                          W.qbad, LOOKUP_Q_RMAX * LOOKUP_Q_RMAX));
                 LAUNCH_CHECK("stats_kernel");
             }
         }
@@ -878,8 +914,9 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
     const size_t tile_smem = (size_t)L * TILE_J * sizeof(float);
     const bool use_smem = tile_smem + lookup_ring_bytes() <= (size_t)LOOKUP_SMEM_MAX;
     const size_t lk_smem = (use_smem ? tile_smem : 0) + lookup_ring_bytes();
-    if (use_smem) CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
-    else CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
+    if (q16) CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
+    else if (use_smem) CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
+    else CUDA_TRY(cudaFuncSetAttribute(lookup_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lk_smem));
     const bool gser = knn_use_gser(Lk, tau);
     if (cv) return conv_blocks(ds, W, offE, T_lib, maskS, tau, m_hi, mode, exclude_self, row_sexp, nlib, ntiles, Np,
                                use_smem, lk_smem, rho, extra, *cv, to, tdist, cs);
@@ -924,9 +961,11 @@ edm_status ccm_core(edm_dataset ds, const int32_t* E, int32_t tau, int m_lo, int
             Q.tau = tau; Q.B = nb; Q.N = N;
             Q.rho = rho; Q.rstride = (int64_t)nlag * N; Q.roff = (int64_t)(l - lag_min) * N;
             Q.rbase = 0; Q.Eok = ECAP;
-            lookup_split(ntiles, nb, sc, Q);
-            if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
-            else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+            Q.Yq = W.Yq; Q.statsq = W.statsq + so; Q.qbad = W.qbad;
+            lookup_split(ntl, nb, sc, Q);
+            if (q16) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true, true><<<ntl + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+            else if (use_smem) PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<true, false><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
+            else PROF_LAUNCH(EDM_PROF_LOOKUP, cs, lookup_kernel<false, false><<<ntiles + Q.nsplit * (Q.parts - 1), LOOKUP_WARPS * 32, lk_smem, cs>>>(Q));
             LAUNCH_CHECK("lookup_kernel");
         }
     }
@@ -941,7 +980,7 @@ edm_status edm_ccm_all_pairs(edm_dataset ds, const int32_t* E, int32_t tau, int3
                              int32_t exclude_self, int32_t lib_begin, int32_t lib_end, float* rho, void* workspace,
                              size_t ws_bytes, void* stream) {
     if (!ds.data || !E || !rho || !workspace) return fail(EDM_EINVAL, "null pointer");
-    if (ds.N < 1 || ds.L < 2 || ds.ld < ds.N || tau < 1 || Tp < 0 || (mode != EDM_E_TARGET && mode != EDM_E_LIBRARY))
+    if (ds.N < 1 || ds.L < 2 || ds.ld < ds.N || tau < 1 || Tp < 0 || !mode_ok(mode, true))
         return fail(EDM_EINVAL, "bad arguments N=%d L=%d ld=%lld tau=%d Tp=%d mode=%d", ds.N, ds.L, (long long)ds.ld, tau, Tp, (int)mode);
     if (lib_begin < 0 || lib_end > ds.N || lib_begin > lib_end) return fail(EDM_EINVAL, "bad library range [%d,%d)", lib_begin, lib_end);
     const size_t need = edm_workspace_bytes(1, ds.N, ds.L, ECAP, tau, Tp);
@@ -954,7 +993,7 @@ edm_status edm_ccm_rows(edm_dataset ds, const int32_t* E, int32_t tau, int32_t T
                         size_t ws_bytes, void* stream) {
     if (!ds.data || !E || !rho || !workspace || (nlib > 0 && !lib_list)) return fail(EDM_EINVAL, "null pointer");
     if (ds.N < 1 || ds.L < 2 || ds.ld < ds.N || tau < 1 || Tp < 0 || nlib < 0 || nlib > ds.N ||
-        (mode != EDM_E_TARGET && mode != EDM_E_LIBRARY))
+        !mode_ok(mode, true))
         return fail(EDM_EINVAL, "bad arguments N=%d L=%d ld=%lld tau=%d Tp=%d nlib=%d mode=%d", ds.N, ds.L, (long long)ds.ld,
                     tau, Tp, nlib, (int)mode);
     for (int r = 0; r < nlib; ++r)
@@ -976,7 +1015,7 @@ edm_status edm_ccm_lagged(edm_dataset ds, const int32_t* E, int32_t tau, int32_t
                           void* workspace, size_t ws_bytes, void* stream) {
     if (!ds.data || !E || !rho || !workspace) return fail(EDM_EINVAL, "null pointer");
     if (ds.N < 1 || ds.L < 2 || ds.ld < ds.N || tau < 1 || lag_min > lag_max ||
-        (mode != EDM_E_TARGET && mode != EDM_E_LIBRARY))
+        !mode_ok(mode, true))
         return fail(EDM_EINVAL, "bad arguments N=%d L=%d ld=%lld tau=%d lags [%d,%d] mode=%d", ds.N, ds.L,
                     (long long)ds.ld, tau, lag_min, lag_max, (int)mode);
     if (lib_begin < 0 || lib_end > ds.N || lib_begin > lib_end) return fail(EDM_EINVAL, "bad library range [%d,%d)", lib_begin, lib_end);

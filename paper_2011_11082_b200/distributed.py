@@ -171,8 +171,8 @@ class _nullctx:
         return False
 
 
-def libccm_phase_fns():
-    """The production phase functions (libccm CUDA path)."""
+def libccm_phase_fns(lookup: str = "fp32"):
+    """The production phase functions (libccm CUDA path); lookup="u16": EDM_LOOKUP_U16."""
     from . import libccm
 
     def simplex_fn(data, E_max, tau, s0, s1):
@@ -181,16 +181,17 @@ def libccm_phase_fns():
     def ccm_fn(data, E, tau, Tp, mode, excl, rows):
         if _is_range(rows):  # contiguous block: the range call
             l0 = int(rows[0]) if rows.size else 0
-            return libccm.ccm_all_pairs(data, E, tau, Tp, mode, excl, l0, l0 + int(rows.size))
-        return libccm.ccm_rows(data, E, rows, tau, Tp, mode, excl)
+            return libccm.ccm_all_pairs(data, E, tau, Tp, mode, excl, l0, l0 + int(rows.size), lookup=lookup)
+        return libccm.ccm_rows(data, E, rows, tau, Tp, mode, excl, lookup=lookup)
 
     return simplex_fn, ccm_fn
 
 
 def causal_map_distributed_to_host(data: torch.Tensor, rho_host: Optional[torch.Tensor], E_max: int = 20, tau: int = 1,
-                                   Tp: int = 1, mode="target", exclude_self: bool = True, nchunk: int = 4, group=None):
+                                   Tp: int = 1, mode="target", exclude_self: bool = True, nchunk: int = 4, group=None,
+                                   lookup: str = "fp32"):
     """Production entry with the map delivered to (page-locked) host memory on rank 0."""
-    sf, cf = libccm_phase_fns()
+    sf, cf = libccm_phase_fns(lookup)
     return run_to_host(data, E_max, tau, Tp, mode, exclude_self, sf, cf, rho_host, nchunk, group)
 
 

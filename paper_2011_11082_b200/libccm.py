@@ -28,6 +28,7 @@ from . import build as _build
 
 EDM_OK, EDM_EINVAL, EDM_ETOOSHORT, EDM_EWORKSPACE, EDM_ECUDA, EDM_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 EDM_E_TARGET, EDM_E_LIBRARY = 0, 1
+EDM_LOOKUP_U16 = 0x100  # OR-ed into mode: 16-bit lookup targets (include/libccm.h)
 E_CAP = 20
 
 EXPORTS = ("edm_embed_knn", "edm_simplex_optimal_E", "edm_ccm_all_pairs", "edm_workspace_bytes",
@@ -186,18 +187,22 @@ def simplex_optimal_E(data: torch.Tensor, E_max: int = 20, tau: int = 1, s_begin
     return (optE, rhoE) if return_rho else optE
 
 
-def _mode(mode) -> int:
+def _mode(mode, lookup: str = "fp32") -> int:
+    if lookup not in ("fp32", "u16"):
+        raise ValueError(f"lookup must be 'fp32' or 'u16', got {lookup!r}")
+    flag = EDM_LOOKUP_U16 if lookup == "u16" else 0
     if mode in ("target", EDM_E_TARGET):
-        return EDM_E_TARGET
+        return EDM_E_TARGET | flag
     if mode in ("library", EDM_E_LIBRARY):
-        return EDM_E_LIBRARY
+        return EDM_E_LIBRARY | flag
     raise ValueError(f"mode must be 'target' or 'library', got {mode!r}")
 
 
 def ccm_all_pairs(data: torch.Tensor, E: torch.Tensor, tau: int = 1, Tp: int = 1, mode="target",
                   exclude_self: bool = True, lib_begin: int = 0, lib_end: Optional[int] = None,
-                  out: Optional[torch.Tensor] = None) -> torch.Tensor:
-    """Phase 2: rho[i - lib_begin, j] for library rows [lib_begin, lib_end) and all targets j."""
+                  out: Optional[torch.Tensor] = None, lookup: str = "fp32") -> torch.Tensor:
+    """Phase 2: rho[i - lib_begin, j] for library rows [lib_begin, lib_end) and all targets j.
+    lookup="u16": the opt-in 16-bit lookup targets (EDM_LOOKUP_U16, include/libccm.h)."""
     ds = _dataset(data)
     _require_cuda(E, torch.int32, "E")
     E = E.contiguous()
@@ -212,13 +217,13 @@ def ccm_all_pairs(data: torch.Tensor, E: torch.Tensor, tau: int = 1, Tp: int = 1
         if not out.is_contiguous() or out.numel() < rows * ds.N:
             raise ValueError("out must be contiguous with at least rows*N elements")
     ws = workspace(1, ds.N, ds.L, E_CAP, tau, Tp, data.device)
-    _check(load().edm_ccm_all_pairs(ds, E.data_ptr(), tau, Tp, _mode(mode), int(exclude_self), lib_begin, lib_end,
+    _check(load().edm_ccm_all_pairs(ds, E.data_ptr(), tau, Tp, _mode(mode, lookup), int(exclude_self), lib_begin, lib_end,
                                     out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(data.device)))
     return out
 
 
 def ccm_rows(data: torch.Tensor, E: torch.Tensor, lib_list, tau: int = 1, Tp: int = 1, mode="target",
-             exclude_self: bool = True, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+             exclude_self: bool = True, out: Optional[torch.Tensor] = None, lookup: str = "fp32") -> torch.Tensor:
     """Phase 2 for a list of library rows (edm_ccm_rows): rho[r, j] for library lib_list[r]."""
     ds = _dataset(data)
     _require_cuda(E, torch.int32, "E")
@@ -232,14 +237,14 @@ def ccm_rows(data: torch.Tensor, E: torch.Tensor, lib_list, tau: int = 1, Tp: in
     elif not out.is_contiguous() or out.numel() < rows * ds.N or out.dtype != torch.float32:
         raise ValueError("out must be a contiguous float32 tensor with at least rows*N elements")
     ws = workspace(1, ds.N, ds.L, E_CAP, tau, Tp, data.device)
-    _check(load().edm_ccm_rows(ds, E.data_ptr(), tau, Tp, _mode(mode), int(exclude_self), lst.ctypes.data if rows else None,
+    _check(load().edm_ccm_rows(ds, E.data_ptr(), tau, Tp, _mode(mode, lookup), int(exclude_self), lst.ctypes.data if rows else None,
                                rows, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(data.device)))
     return out
 
 
 def ccm_lagged(data: torch.Tensor, E: torch.Tensor, tau: int = 1, lag_min: int = -2, lag_max: int = 2,
                mode="target", exclude_self: bool = True, lib_begin: int = 0, lib_end: Optional[int] = None,
-               out: Optional[torch.Tensor] = None) -> torch.Tensor:
+               out: Optional[torch.Tensor] = None, lookup: str = "fp32") -> torch.Tensor:
     """Time-delay cross mapping (edm_ccm_lagged): rho [rows, nlags, N] for lags lag_min..lag_max
     from one set of kNN tables per library block."""
     ds = _dataset(data)
@@ -255,7 +260,7 @@ def ccm_lagged(data: torch.Tensor, E: torch.Tensor, tau: int = 1, lag_min: int =
     if nbytes == 0:
         raise EdmError(EDM_EINVAL, f"bad lagged workspace request N={ds.N} L={ds.L} lags=[{lag_min},{lag_max}]")
     ws = _workspace_for("lagged", nbytes, data.device)
-    _check(load().edm_ccm_lagged(ds, E.data_ptr(), tau, lag_min, lag_max, _mode(mode), int(exclude_self), lib_begin,
+    _check(load().edm_ccm_lagged(ds, E.data_ptr(), tau, lag_min, lag_max, _mode(mode, lookup), int(exclude_self), lib_begin,
                                  lib_end, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream(data.device)))
     return out
 
@@ -331,15 +336,16 @@ def ccm_tables(data: torch.Tensor, E: torch.Tensor, Eq: int, tau: int = 1, lag_m
 
 
 def causal_map(data: torch.Tensor, E_max: int = 20, tau: int = 1, Tp: int = 1, mode="target",
-               exclude_self: bool = True):
+               exclude_self: bool = True, lookup: str = "fp32"):
     """Both phases on one GPU from a device-resident dataset -> (optE, rho [N, N])."""
     optE = simplex_optimal_E(data, E_max, tau)
-    rho = ccm_all_pairs(data, optE, tau, Tp, mode, exclude_self)
+    rho = ccm_all_pairs(data, optE, tau, Tp, mode, exclude_self, lookup=lookup)
     return optE, rho
 
 
 def causal_map_host(data: np.ndarray, E_max: int = 20, tau: int = 1, Tp: int = 1, mode="target",
-                    exclude_self: bool = True, rho_out: Optional[np.ndarray] = None, with_rhoE: bool = False):
+                    exclude_self: bool = True, rho_out: Optional[np.ndarray] = None, with_rhoE: bool = False,
+                    lookup: str = "fp32"):
     """End-to-end from host memory through edm_causal_map_host (H2D, both phases, D2H)."""
     data = np.ascontiguousarray(data, dtype=np.float32)
     L, N = data.shape
@@ -347,7 +353,7 @@ def causal_map_host(data: np.ndarray, E_max: int = 20, tau: int = 1, Tp: int = 1
     rho = rho_out if rho_out is not None else np.empty((N, N), np.float32)
     assert rho.dtype == np.float32 and rho.flags.c_contiguous and rho.size >= N * N
     rhoE = np.empty((N, E_max), np.float32) if with_rhoE else None
-    _check(load().edm_causal_map_host(data.ctypes.data, N, L, E_max, tau, Tp, _mode(mode), int(exclude_self),
+    _check(load().edm_causal_map_host(data.ctypes.data, N, L, E_max, tau, Tp, _mode(mode, lookup), int(exclude_self),
                                       optE.ctypes.data, rho.ctypes.data, rhoE.ctypes.data if with_rhoE else None))
     return (optE, rho, rhoE) if with_rhoE else (optE, rho)
 
