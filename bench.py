@@ -512,6 +512,8 @@ def main():
         "peak_source": f"derived: {nsm} SMs x 128 B/clk x {sm_max_mhz:.0f} MHz (B300_MICROARCH smem crossbar; "
                        "MEASURED_PEAKS.json has no smem figure -- the measured one is peak_measured)",
         "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_s * 1e3, "launches": lk_n,
+        "algorithmic_note": ("--lookup u16: algorithmic bytes counted at the fp32 definition (4 B per gathered or "
+                             "observed value, SURVEY 8(d)); the 16-bit codes move 2 B each") if args.lookup == "u16" else None,
         "share_of_step": lk_ms / ms_local if ms_local else None,
         "pipe_model": {"frac": (lookup_pipe_cycles(E_host, L, tau, Tp, args.mode) * (0.5 if args.lookup == "u16" else 1.0)
                                 * rows_frac * nlag * args.steps /

@@ -916,7 +916,7 @@ struct LookupParams {
 #define CCM_LK_STAGES 2
 #endif
 #ifndef CCM_LK_UNROLL
-#define CCM_LK_UNROLL 4
+#define CCM_LK_UNROLL 8
 #endif
 constexpr int LK_CHUNK = CCM_LK_CHUNK;    // bytes per stage
 constexpr int LK_STAGES = CCM_LK_STAGES;
@@ -1071,6 +1071,10 @@ __device__ __forceinline__ float2 lk_codes(uint32_t w) {
                        __uint_as_float(__byte_perm(w, 0x3F000000u, 0x7324)));
 }
 
+#ifndef CCM_LKQ_UNROLL
+#define CCM_LKQ_UNROLL 16
+#endif
+constexpr int LKQ_UNROLL = CCM_LKQ_UNROLL;  // rows in flight per warp (16-bit lookup)
 template <int E>
 __device__ __forceinline__ void lookup_one_q(const LookupParams& P, const float* __restrict__ Y, int tile, int b,
                                              int lane, int col0, int col1, WarpRing& R) {
@@ -1105,7 +1109,7 @@ __device__ __forceinline__ void lookup_one_q(const LookupParams& P, const float*
         const uint4* rowp = R.buf + slot * (LK_CHUNK / 16);
         const int r0 = ci * ROWS, r1 = min(n, r0 + ROWS);
         float2 sp = make_float2(0.f, 0.f), spp = sp, spo = sp;
-#pragma unroll LK_UNROLL
+#pragma unroll LKQ_UNROLL
         for (int r = r0; r < r1; ++r) {
             const uint4* row = rowp + (r - r0) * (kp / 2);
             float2 p = make_float2(0.f, 0.f);
