@@ -196,7 +196,7 @@ def causal_map_distributed_to_host(data: torch.Tensor, rho_host: Optional[torch.
 
 
 def causal_map_distributed(data: torch.Tensor, E_max: int = 20, tau: int = 1, Tp: int = 1, mode="target",
-                           exclude_self: bool = True, gather: bool = True, group=None):
+                           exclude_self: bool = True, gather: bool = True, group=None, lookup: str = "fp32"):
     """Production entry: every rank passes the full dataset on its own GPU."""
-    sf, cf = libccm_phase_fns()
+    sf, cf = libccm_phase_fns(lookup)
     return run(data, E_max, tau, Tp, mode, exclude_self, sf, cf, gather, group)

@@ -22,6 +22,7 @@ from paper_2011_11082_b200 import distributed, libccm, synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--N", type=int, default=None)
+ap.add_argument("--lookup", default="fp32", choices=["fp32", "u16"])
 a = ap.parse_args()
 local = int(os.environ.get("LOCAL_RANK", "0"))
 torch.cuda.set_device(local)
@@ -31,14 +32,14 @@ rank, world = dist.get_rank(), dist.get_world_size()
 libccm.load()
 data = torch.from_numpy(synth.make_config(a.config, N=a.N)).to(dev)
 L, N = data.shape
-out = {"config": a.config, "N": N, "L": L, "world": world}
+out = {"config": a.config, "N": N, "L": L, "world": world, "lookup": a.lookup}
 for mode in ("target", "library"):
     t0 = time.time()
-    E, rows, full = distributed.causal_map_distributed(data, 20, 1, 1, mode, True)
+    E, rows, full = distributed.causal_map_distributed(data, 20, 1, 1, mode, True, lookup=a.lookup)
     torch.cuda.synchronize()
     out[f"{mode}_distributed_s"] = time.time() - t0
     if rank == 0:
-        E1, rho1 = libccm.causal_map(data, 20, 1, 1, mode, True)
+        E1, rho1 = libccm.causal_map(data, 20, 1, 1, mode, True, lookup=a.lookup)
         torch.cuda.synchronize()
         out[f"{mode}_optE_identical"] = bool(torch.equal(E.cpu(), E1.cpu()))
         out[f"{mode}_map_identical"] = bool(torch.equal(full.view(torch.int32), rho1.view(torch.int32)))
