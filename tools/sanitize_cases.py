@@ -41,6 +41,14 @@ os.environ["CCM_KNN_ALGO"] = "sweep"
 libccm.simplex_optimal_E(d, 8)
 libccm.ccm_all_pairs(d, E, 1, 1, "target")
 del os.environ["CCM_KNN_ALGO"]
+# 16-bit lookup targets: the code path, and a flagged 64-tile (heavy tail) on the fp32 fallback
+libccm.ccm_all_pairs(d, E, 1, 1, "target", lookup="u16")
+libccm.ccm_all_pairs(d, E, 1, 0, "library", lookup="u16")
+libccm.ccm_lagged(d, E, 1, -2, 2, "target", lookup="u16")
+ht = synth.make_config("c2", N=150, L=200)
+ht[50, 100] += 1e3
+dh = dev(ht)
+libccm.ccm_all_pairs(dh, libccm.simplex_optimal_E(dh, 6), 1, 1, "library", lookup="u16")
 long = dev(synth.make_config("c5", N=12, L=2100))  # target tiles beyond shared memory: global gathers
 libccm.ccm_all_pairs(long, dev(np.arange(1, 13) % 6 + 1, torch.int32), 1, 1, "target", True, 0, 3)
 torch.cuda.synchronize()
